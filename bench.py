@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark: trained words/sec of skip-gram HS training (BASELINE.json metric).
+
+A "step" is one training pass of the hot path over one GPU's shard of the synthetic
+corpus (default: BASELINE config 2, the text8-shaped 17M-token Zipf(1.05) corpus,
+V 71k, D 200, W 5, sample 1e-4, K 31). Inputs (id stream, tree, model) are resident
+in HBM before the timed region. Each timed step = K3 subsampling/pair generation +
+K1 Hogwild training (+ periodic all-reduce averaging at N > 1).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Under torchrun each rank trains its own shard (weak scaling) on its own GPU and
+averages syn0/syn1 with NCCL every --sync-words words. Rank 0 prints ONE JSON line.
+`--impl reference` times the reference's own CPU implementation (the reference headers
+compiled unchanged, oracle/_ref) on this host's cores on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "trained words/sec (skip-gram HS)"
+UNIT = "words/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--cache-nodes", type=int, default=31)
+    p.add_argument("--sync-words", type=int, default=1_000_000, help="all-reduce interval per GPU (N > 1)")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--cpu-sample-tokens", type=int, default=0, help="reference sample size (0 = auto)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--warps", type=int, default=0)
+    p.add_argument("--cpw", type=int, default=0)
+    p.add_argument("--rows", type=int, default=-1)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ workload
+def workload(cfg_name: str, rank: int, world: int):
+    """Per-rank shard of the configured corpus plus the shared vocabulary/tree.
+    Each rank's shard has the configuration's full token count (weak scaling) and is
+    drawn with its own seed; the vocabulary comes from shard 0 with ties broken by
+    raw rank, so every rank builds the identical tree without communication."""
+    from paper_1606_07822_b200.corpus_gen import CONFIGS, cluster_raw_ids, vocab_from_raw, zipf_raw_ids
+
+    c = CONFIGS[cfg_name]
+    if c.clusters:
+        raw0, _ = cluster_raw_ids(c)
+        space = c.clusters * c.cluster_size
+    else:
+        raw0 = zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed)
+        space = c.vocab
+    vocab, ids0 = vocab_from_raw(raw0, c.min_count, space)
+    if rank == 0:
+        ids = ids0
+    else:
+        raw = zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed * 1000 + rank) if not c.clusters else raw0
+        rank_of = np.full(space, -1, np.int32)
+        rank_of[vocab.raw_of_id] = np.arange(vocab.size(), dtype=np.int32)
+        ids = rank_of[raw]
+        ids = np.ascontiguousarray(ids[ids >= 0])
+    return c, vocab, ids
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[3:7]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm / CPU baseline
+def reference_sample(c, vocab, ids, sample_tokens: int, workdir: str):
+    """Writes the first `sample_tokens` tokens of the id stream as text (`w<id>`, newline
+    every 1000) for the reference's file-based train(); its vocabulary is built from the
+    full-corpus counts so keep probabilities and the tree match the GPU run."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import ctypes as C
+
+    import oracle_lib as O
+
+    n = min(sample_tokens, ids.size)
+    path = os.path.join(workdir, f"ref_sample_{c.name}.txt")
+    words = np.array([b"w%d" % i for i in range(vocab.size())], dtype=object)
+    with open(path, "wb") as f:
+        for a in range(0, n, 1_000_000):
+            toks = words[ids[a:min(n, a + 1_000_000)]]
+            f.write(b"\n".join(b" ".join(toks[i:i + 1000].tolist()) for i in range(0, toks.size, 1000)) + b"\n")
+    counts = np.ascontiguousarray(vocab.counts, np.int64)
+    h = O.ref().ref_open_counts(counts.ctypes.data_as(C.POINTER(C.c_int64)), counts.size)
+    return O, h, path, n
+
+
+def run_reference(c, vocab, ids, threads: int, sample_tokens: int, reps: int, cache_nodes: int):
+    with tempfile.TemporaryDirectory() as d:
+        O, h, path, n = reference_sample(c, vocab, ids, sample_tokens, d)
+        cfg = dict(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1, cache_nodes=cache_nodes,
+                   flush_interval=10, seed=c.seed)
+        rates, walls = [], []
+        for _ in range(reps):
+            _, _, words, wall = O.ref_train(h, path, cfg, workers=threads)
+            rates.append(words / wall)
+            walls.append(wall)
+        O.ref().ref_close(h)
+    return rates, walls, n
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def auto_sample(c) -> int:
+    # ~10-30 s of reference CPU work on a many-core host; scaled by D*L per word
+    per_word = {"c1": 1.0, "c2": 2.0, "c3": 3.0, "c4": 6.0, "c5": 1.0}[c.name]
+    return int(min(c.tokens, 4_000_000 / per_word))
+
+
+# ------------------------------------------------------------------ main
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        c, vocab, ids = workload(args.config, 0, 1)
+        threads = cpu_threads()
+        sample = args.cpu_sample_tokens or auto_sample(c)
+        for _ in range(max(args.warmup, 0) and 1):
+            run_reference(c, vocab, ids, threads, min(sample, 200_000), 1, args.cache_nodes)
+        rates, walls, n = run_reference(c, vocab, ids, threads, sample, args.steps, args.cache_nodes)
+        words = n * args.steps
+        value = words / sum(walls)
+        line = {
+            "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(walls) / len(walls),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {c.tokens // 10**6}M-token Zipf({c.zipf_s}) V {vocab.size()} "
+                                   f"D {c.dim} W {c.window} sample {c.sample} K {args.cache_nodes}",
+                       "sample_tokens_per_step": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"first {n} tokens of the {args.config} corpus, 1 pass per step, "
+                                       f"reference train() with workers={threads}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1606_07822_b200 import api
+
+    c, vocab, ids = workload(args.config, rank, world)
+    tree = api.build_huffman_tree(vocab)
+    sel = api.select_cached_nodes(tree, args.cache_nodes)
+    cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
+                          cache_nodes=args.cache_nodes, seed=c.seed)
+    stream = torch.cuda.current_stream()
+    sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
+    sess.tune(args.warps, args.cpw, args.rows)
+    sess.upload_ids(ids)
+    model_t = sess.model_tensor() if world > 1 else None
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    T = ids.size
+    chunks = [(a, min(T, a + args.sync_words)) for a in range(0, T, args.sync_words)] if world > 1 else [(0, T)]
+    launches = {"n": 0}
+    agg = {"train_ms": 0.0, "bytes": 0.0, "pairs": 0, "steps": 0, "kept": 0, "launch_count": 0}
+
+    def one_step(epoch: int, record: bool):
+        for a, b in chunks:
+            e = sess.train_range(epoch, a, b, progress_base=a * world, progress_mult=world)
+            if record:
+                launches["n"] += e.train_launches + e.other_launches
+                agg["train_ms"] += e.train_ms
+                agg["bytes"] += 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs)
+                agg["pairs"] += e.pairs
+                agg["steps"] += e.steps
+                agg["kept"] += e.kept
+                agg["launch_count"] += e.train_launches
+            if world > 1:
+                dist.all_reduce(model_t, op=dist.ReduceOp.AVG)
+
+    for w in range(args.warmup):
+        one_step(10_000 + w, False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    step_ms = []
+    for s in range(args.steps):
+        l2_flush.fill_(float(s))  # > L2 (126 MB): evicts the previous step's lines
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        one_step(s, True)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    words_all = float(T) * args.steps * world  # every rank's shard has the same size
+    value = words_all / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (K1 hs_train): algorithmic bytes per launch / launch time
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    n_launch = max(agg["launch_count"], 1)
+    per_launch_bytes = agg["bytes"] / n_launch
+    per_launch_ms = agg["train_ms"] / n_launch
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # end to end through the public API: host ids in (pinned), host model out (pinned)
+    e2e = None
+    if args.e2e_steps > 0:
+        ids_pin = torch.from_numpy(ids).pin_memory()
+        out0 = torch.empty((vocab.size(), c.dim), dtype=torch.float32).pin_memory()
+        out1 = torch.empty((vocab.size() - 1, c.dim), dtype=torch.float32).pin_memory()
+        from paper_1606_07822_b200._lib import CgTrainStats, check, load, ptr
+        import ctypes as C
+
+        keep: list = []
+        desc = api.model_desc(vocab, tree, sel, keep)
+        ccfg = cfg.to_c()
+        walls = []
+        for _ in range(args.e2e_steps):
+            st = CgTrainStats()
+            t0 = time.perf_counter()
+            check(load().cg_train(C.byref(ccfg), 0, C.byref(desc), ptr(ids_pin.numpy(), C.c_int32), T,
+                                  ptr(out0.numpy(), C.c_float), ptr(out1.numpy(), C.c_float), C.byref(st)))
+            walls.append(time.perf_counter() - t0)
+        e2e_wall = float(np.median(walls))
+        if world > 1:
+            t = torch.tensor([e2e_wall], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_wall = float(t.item())
+        e2e = {"value": float(T) * world / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": int(ids.nbytes),
+               "d2h_bytes_per_step": int(out0.numel() * 4 + out1.numel() * 4),
+               "note": "cg_train(): host ids -> device, model init, subsample + train, device -> host model"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = cpu_threads()
+            sample = args.cpu_sample_tokens or auto_sample(c)
+            rates, walls, n = run_reference(c, vocab, ids, threads, sample, 1, args.cache_nodes)
+            cpu = {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"first {n} tokens of the {args.config} corpus, 1 pass, reference train() "
+                             f"(headers compiled unchanged, -O3) with workers={threads}"}
+        except Exception as ex:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference", "sample": f"failed: {ex}"}
+
+    sess.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {c.tokens / 1e6:g}M-token Zipf({c.zipf_s}) per GPU, V {vocab.size()}, "
+                                   f"D {c.dim}, W {c.window}, sample {c.sample}, K {args.cache_nodes}, 1 pass per step",
+                       "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}",
+                       "sync_words_per_gpu": args.sync_words if world > 1 else None},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "hog_kernel (K1)", "algorithmic_bytes_per_launch": per_launch_bytes,
+                         "kernel_ms_per_launch": per_launch_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches["n"],
+            "clocks": clk,
+            "detail": {"pairs_per_step": agg["pairs"] / args.steps, "path_steps_per_step": agg["steps"] / args.steps,
+                       "kept_per_step": agg["kept"] / args.steps, "step_ms": step_ms},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,195 @@
+/*
+ * cachegram_b200.h -- the C-ABI of libcachegram_b200.so.
+ *
+ * This is the drop-in boundary for the reference's hot path, cachegram::train()
+ * (/root/reference/proj/include/cachegram/trainer.hpp:254-316). Plain C types only:
+ * pointers, sizes and status codes; no C++ or torch types cross it. The C++ API in
+ * include/cachegram/trainer.hpp (same names as the reference) and the Python package
+ * (ctypes) are both thin layers over these entry points; INTEGRATION.md shows the
+ * binding a maintainer of the reference would add.
+ *
+ * Status codes map onto the reference's exceptions (trainer.hpp:37-47, 256-260;
+ * corpus.hpp:194,232; errors.hpp:12-24): CG_ERR_INVALID_ARGUMENT -> std::invalid_argument,
+ * CG_ERR_IO -> IoError, CG_ERR_NO_TRAINABLE_WORDS -> NoTrainableWords, the rest ->
+ * std::runtime_error. The message is in cg_last_error() (thread-local).
+ *
+ * Everything that computes on the training path runs on the GPU; there is no CPU
+ * fallback. Without a usable CUDA device the training entry points return CG_ERR_CUDA.
+ */
+#ifndef CACHEGRAM_B200_H
+#define CACHEGRAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CG_ABI_VERSION 1
+
+/* The library is built with -fvisibility=hidden; only these entry points are exported. */
+#if defined(__GNUC__)
+#define CG_API __attribute__((visibility("default")))
+#else
+#define CG_API
+#endif
+
+enum cg_status {
+    CG_OK = 0,
+    CG_ERR_INVALID_ARGUMENT = 1,
+    CG_ERR_IO = 2,
+    CG_ERR_CUDA = 3,
+    CG_ERR_NCCL = 4,
+    CG_ERR_NO_TRAINABLE_WORDS = 5,
+    CG_ERR_INTERNAL = 6
+};
+
+/* Training modes. DETERMINISTIC replays the reference's single-worker stream
+ * (trainer.hpp:200-245 with workers == 1: same RNG draws, same sentence chunks, same
+ * node-cache flush points, sequential non-fused fp32 arithmetic) on one warp and is
+ * bit-identical to the reference. HOGWILD is the throughput path: device-side
+ * subsampling and pair generation, thousands of warps updating one device-resident
+ * model lock-free, with a per-block shared-memory cache of the hot inner-node rows. */
+enum cg_mode { CG_MODE_HOGWILD = 0, CG_MODE_DETERMINISTIC = 1 };
+
+/* Mirrors cachegram::TrainConfig (trainer.hpp:25-35), field for field. */
+typedef struct cg_config {
+    int32_t dim;
+    int32_t window;
+    int64_t min_count;
+    double sample;
+    float alpha0;
+    int32_t iterations;
+    int32_t workers;        /* reference CPU thread count; the GPU path ignores it */
+    int32_t cache_nodes;    /* K */
+    int32_t flush_interval; /* u, in trained centers (deterministic mode) */
+    uint64_t seed;
+} cg_config;
+
+/* What train() receives besides the corpus: Vocabulary counts, the HuffmanTree paths
+ * (root-first CSR, huffman.hpp:30-52) and the CacheSelection (huffman.hpp:116-134). */
+typedef struct cg_model_desc {
+    int32_t vocab_size;          /* V >= 2 */
+    const int64_t* counts;       /* [V]   Vocabulary::count, ids in vocabulary order */
+    int64_t total_tokens;        /* Vocabulary::total_tokens */
+    const int64_t* path_offsets; /* [V+1] */
+    const int32_t* path_nodes;   /* [path_offsets[V]] inner node ids 0..V-2 */
+    const uint8_t* path_turns;   /* [path_offsets[V]] 0/1 */
+    const int64_t* node_usage;   /* [V-1] HuffmanTree::node_usage */
+    const int32_t* hot_nodes;    /* [hot_count] CacheSelection slot order; may be NULL if hot_count == 0 */
+    int32_t hot_count;           /* CacheSelection::size() = min(K, V-1) */
+} cg_model_desc;
+
+typedef struct cg_train_stats {
+    uint64_t words_processed; /* in-vocabulary tokens read, all iterations (trainer.hpp:178) */
+    double wall_seconds;      /* host wall time of the training loop (trainer.hpp:280-307) */
+    double words_per_second;
+    double kernel_seconds;    /* summed device time of the training kernels (CUDA events) */
+    uint64_t centers;         /* kept centers trained */
+    uint64_t pairs;           /* (center, context) pairs trained */
+    uint64_t steps;           /* pair x path-step updates */
+} cg_train_stats;
+
+/* ---- library --------------------------------------------------------------- */
+CG_API int cg_abi_version(void);
+CG_API const char* cg_last_error(void);
+/* Number of visible CUDA devices (0 when none); never falls back. */
+CG_API int cg_device_count(void);
+
+/* ---- host pieces of the path (reference algorithms, C-ABI for FFI callers) ---- */
+/* corpus.hpp:176-181 */
+CG_API double cg_keep_probability(int64_t count, int64_t total_tokens, double sample);
+/* trainer.hpp:58-63 */
+CG_API float cg_update_alpha(uint64_t words_processed, uint64_t total_words, float alpha0);
+/* model.hpp:84-91: out[1000] */
+CG_API void cg_sigmoid_table(float* out);
+/* model.hpp:66-72: syn0 [V*D] (syn1 is all zeros) */
+CG_API int cg_init_model(int32_t vocab_size, int32_t dim, uint64_t seed, float* syn0);
+/* huffman.hpp:57-108. Two calls: with path_nodes == NULL only *n_steps is written. */
+CG_API int cg_build_huffman(const int64_t* counts, int32_t vocab_size, int64_t* path_offsets, int32_t* path_nodes,
+                     uint8_t* path_turns, int64_t* node_usage, int64_t* n_steps);
+/* huffman.hpp:139-159. Returns the selection size, or -1 (see cg_last_error). */
+CG_API int32_t cg_select_cached_nodes(const int64_t* node_usage, int32_t inner_count, int32_t k, int32_t* hot_nodes,
+                               int32_t* slot_of);
+/* corpus.hpp:136-170 + trainer.hpp:220-222: vocabulary of a corpus file, then the file as an
+ * in-vocabulary id stream. Two-phase: cg_corpus_open -> query/export -> cg_corpus_close. */
+typedef struct cg_corpus cg_corpus;
+CG_API int cg_corpus_open(const char* path, int64_t min_count, cg_corpus** out);
+CG_API int32_t cg_corpus_vocab_size(const cg_corpus* c);
+CG_API int64_t cg_corpus_total_tokens(const cg_corpus* c);
+CG_API int64_t cg_corpus_word_bytes(const cg_corpus* c); /* sum of word lengths + V (NUL separators) */
+CG_API int cg_corpus_export_vocab(const cg_corpus* c, int64_t* counts, char* words_nul_separated);
+CG_API int cg_corpus_read_ids(const cg_corpus* c, const char* path, int32_t* ids, int64_t capacity, int64_t* n_ids);
+CG_API void cg_corpus_close(cg_corpus* c);
+
+/* ---- the hot path: cachegram::train() (trainer.hpp:254-316) -------------------
+ * Host buffers in, host buffers out. `ids` is the in-vocabulary id stream of the corpus
+ * (cg_corpus_read_ids). The model starts from init_model(V, dim, seed) exactly as the
+ * reference's train() does (trainer.hpp:262). syn0_out [V*dim] and syn1_out [(V-1)*dim]
+ * receive the trained matrices in reference layout and node order. Blocking. */
+CG_API int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids, int64_t n_ids,
+             float* syn0_out, float* syn1_out, cg_train_stats* stats);
+
+/* ---- kernel-level entry: one train_center() call (trainer.hpp:147-175) ---------
+ * Runs the deterministic device kernel for a single center on host buffers, with the
+ * NodeCache (trainer.hpp:75-138) state passed explicitly: cache_work/cache_snap
+ * [hot_count*dim], cache_flag [hot_count] (1 = acquired). slot_of [V-1] may be NULL
+ * when hot_count == 0. sigmoid_mode: 0 = SigmoidTable, 1 = exact logistic,
+ * 2 = the constant sig_const. *sigmoid_calls receives the number of evaluations. */
+CG_API int cg_train_center(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
+                    int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
+                    const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
+                    const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
+                    uint8_t* cache_flag, float alpha, int32_t sigmoid_mode, float sig_const, int64_t* sigmoid_calls);
+/* NodeCache::flush (trainer.hpp:110-124) on the device: syn1[hot_nodes[s]] += work - snap
+ * for every acquired slot, then clears the flags. */
+CG_API int cg_cache_flush(int32_t vocab_size, int32_t dim, float* syn1, const int32_t* hot_nodes, int32_t hot_count,
+                   float* cache_work, const float* cache_snap, uint8_t* cache_flag);
+
+/* ---- sessions: device-resident training for benchmarks and multi-GPU -----------
+ * A session owns the device copies of the tree, the hot-row selection, the keep
+ * probabilities, the id stream and the model (one buffer: syn0 rows then syn1 rows,
+ * rows padded to a multiple of 4 floats, syn1 rows in usage-rank order). */
+typedef struct cg_session cg_session;
+
+typedef struct cg_epoch_stats {
+    uint64_t words;          /* id-stream tokens covered by this call */
+    uint64_t kept;           /* centers after subsampling */
+    uint64_t pairs;
+    uint64_t steps;
+    double train_ms;         /* device time of the training kernel(s) */
+    double subsample_ms;     /* device time of subsampling + compaction */
+    int32_t train_launches;  /* kernels launched by this call */
+    int32_t other_launches;
+} cg_epoch_stats;
+
+/* stream: a cudaStream_t (NULL = legacy default stream). device: CUDA ordinal. */
+CG_API int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* model, int32_t device, void* stream,
+                      cg_session** out);
+CG_API void cg_session_destroy(cg_session* s);
+/* Copies the host id stream into device memory owned by the session. */
+CG_API int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids);
+/* (Re)initialises the model on the device side from init_model(V, dim, seed). */
+CG_API int cg_session_reset_model(cg_session* s);
+/* Uploads a model given in reference layout (host). */
+CG_API int cg_session_set_model(cg_session* s, const float* syn0, const float* syn1);
+/* One training pass over ids[tok_begin, tok_end). The learning rate follows
+ * update_alpha(progress, iterations * total_tokens) with
+ * progress = progress_base + progress_mult * (tokens read in this range so far),
+ * i.e. progress_mult = N replicas estimate the global counter.
+ * `epoch` decorrelates the counter-based draws of successive passes. Blocking. */
+CG_API int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int64_t tok_end, uint64_t progress_base,
+                           uint32_t progress_mult, cg_epoch_stats* stats);
+/* Whole-run convenience: config.iterations passes over the uploaded ids. */
+CG_API int cg_session_train(cg_session* s, cg_train_stats* stats);
+CG_API int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out);
+/* The device model buffer (for an all-reduce between replicas) and its geometry. */
+CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int32_t* row_stride_floats);
+/* Overrides the hogwild kernel geometry (0 = auto). For tuning and tests. */
+CG_API int cg_session_tune(cg_session* s, int32_t warps_per_block, int32_t centers_per_warp, int32_t smem_cache_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,463 @@
+"""Python mirror of the reference's training interface, over the C-ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/cachegram
+(corpus.hpp, huffman.hpp, model.hpp, trainer.hpp): ``TrainConfig``, ``Vocabulary``,
+``build_vocabulary_file``, ``HuffmanTree``/``build_huffman_tree``, ``CacheSelection``/
+``select_cached_nodes``, ``Model``/``init_model``, ``keep_probability``,
+``update_alpha``, ``NodeCache``, ``train_center`` and ``train``. C++ ``std::invalid_argument``
+surfaces as ``ValueError`` and ``IoError`` as ``OSError``. Every training computation
+runs in libcachegram_b200.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import CgConfig, CgEpochStats, CgModelDesc, CgTrainStats, check, load, ptr
+
+MODES = {"hogwild": _lib.CG_MODE_HOGWILD, "deterministic": _lib.CG_MODE_DETERMINISTIC}
+
+
+# --------------------------------------------------------------------------- config
+@dataclass
+class TrainConfig:
+    """trainer.hpp:25-48 (+ ``mode``: "hogwild" (default) or "deterministic")."""
+    dim: int = 100
+    window: int = 5
+    min_count: int = 5
+    sample: float = 1e-3
+    alpha0: float = 0.025
+    iterations: int = 5
+    workers: int = 1
+    cache_nodes: int = 31
+    flush_interval: int = 10
+    seed: int = 1
+    mode: str = "hogwild"
+
+    def validate(self) -> None:
+        for ok, msg in (
+            (self.dim >= 1, "dim must be >= 1"),
+            (self.window >= 1, "window must be >= 1"),
+            (self.min_count >= 1, "min-count must be >= 1"),
+            (self.sample >= 0.0, "sample must be >= 0"),
+            (self.alpha0 > 0.0, "alpha must be > 0"),
+            (self.iterations >= 1, "iterations must be >= 1"),
+            (self.workers >= 1, "workers must be >= 1"),
+            (self.cache_nodes >= 0, "cache-nodes must be >= 0"),
+            (self.flush_interval >= 1, "flush-interval must be >= 1"),
+        ):
+            if not ok:
+                raise ValueError(msg)
+        if self.mode not in MODES:
+            raise ValueError(f"unknown training mode {self.mode!r}")
+
+    def to_c(self) -> CgConfig:
+        return CgConfig(self.dim, self.window, self.min_count, self.sample, self.alpha0, self.iterations,
+                        self.workers, self.cache_nodes, self.flush_interval, self.seed & 0xFFFFFFFFFFFFFFFF)
+
+
+@dataclass
+class TrainStats:
+    words_processed: int = 0
+    wall_seconds: float = 0.0
+    words_per_second: float = 0.0
+    kernel_seconds: float = 0.0
+    centers: int = 0
+    pairs: int = 0
+    steps: int = 0
+
+
+# --------------------------------------------------------------------------- corpus
+class Vocabulary:
+    """corpus.hpp:55-83: ids 0..V-1 by descending count, first occurrence on ties."""
+
+    def __init__(self, counts: Sequence[int], words: Sequence[str] | None = None, total: int | None = None,
+                 _handle=None):
+        self.counts = np.ascontiguousarray(np.asarray(counts, dtype=np.int64))
+        self.words = list(words) if words is not None else [f"w{i}" for i in range(len(self.counts))]
+        self._index = {w: i for i, w in enumerate(self.words)}
+        self.total = int(self.counts.sum()) if total is None else int(total)
+        self._handle = _handle
+
+    def size(self) -> int:
+        return int(self.counts.shape[0])
+
+    def total_tokens(self) -> int:
+        return self.total
+
+    def count(self, i: int) -> int:
+        return int(self.counts[i])
+
+    def word(self, i: int) -> str:
+        return self.words[i]
+
+    def id_of(self, w: str) -> int:
+        return self._index.get(w, -1)
+
+    def __del__(self):
+        if getattr(self, "_handle", None):
+            load().cg_corpus_close(self._handle)
+            self._handle = None
+
+
+def build_vocabulary_file(path: str, min_count: int) -> Vocabulary:
+    """corpus.hpp:144-170 (C++ host code in the library)."""
+    lib = load()
+    h = C.c_void_p()
+    check(lib.cg_corpus_open(str(path).encode(), int(min_count), C.byref(h)))
+    v = lib.cg_corpus_vocab_size(h)
+    counts = np.zeros(v, dtype=np.int64)
+    buf = C.create_string_buffer(int(lib.cg_corpus_word_bytes(h)) + 1)
+    check(lib.cg_corpus_export_vocab(h, ptr(counts, C.c_int64), buf))
+    words = buf.raw[: lib.cg_corpus_word_bytes(h)].split(b"\0")[:v]
+    return Vocabulary(counts, [w.decode() for w in words], int(lib.cg_corpus_total_tokens(h)), _handle=h)
+
+
+def read_id_stream(path: str, vocab: Vocabulary) -> np.ndarray:
+    """The in-vocabulary id stream of a corpus file (what ShardReader + id_of yield)."""
+    if vocab._handle is None:
+        raise ValueError("vocabulary was not built from a file")
+    lib = load()
+    n = C.c_int64()
+    check(lib.cg_corpus_read_ids(vocab._handle, str(path).encode(), None, 0, C.byref(n)))
+    ids = np.empty(n.value, dtype=np.int32)
+    check(lib.cg_corpus_read_ids(vocab._handle, str(path).encode(), ptr(ids, C.c_int32), n.value, C.byref(n)))
+    return ids
+
+
+def keep_probability(count: int, total_tokens: int, sample: float) -> float:
+    return float(load().cg_keep_probability(int(count), int(total_tokens), float(sample)))
+
+
+def update_alpha(words_processed: int, total_words: int, alpha0: float) -> float:
+    return float(load().cg_update_alpha(int(words_processed), int(total_words), float(alpha0)))
+
+
+def sigmoid_table() -> np.ndarray:
+    t = np.zeros(1000, dtype=np.float32)
+    load().cg_sigmoid_table(ptr(t, C.c_float))
+    return t
+
+
+# --------------------------------------------------------------------------- tree
+class HuffmanTree:
+    """huffman.hpp:30-52: root-first (node, turn) paths as CSR, plus node usage."""
+
+    def __init__(self, offsets: np.ndarray, nodes: np.ndarray, turns: np.ndarray, usage: np.ndarray):
+        self.offsets, self.nodes, self.turns, self.usage = offsets, nodes, turns, usage
+
+    def inner_count(self) -> int:
+        return int(self.usage.shape[0])
+
+    def leaf_count(self) -> int:
+        return int(self.offsets.shape[0]) - 1
+
+    def root_id(self) -> int:
+        return self.inner_count() - 1
+
+    def path(self, w: int) -> list[tuple[int, int]]:
+        a, b = int(self.offsets[w]), int(self.offsets[w + 1])
+        return list(zip(self.nodes[a:b].tolist(), self.turns[a:b].tolist()))
+
+    def node_usage(self, n: int) -> int:
+        return int(self.usage[n])
+
+    def depth(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+
+def build_huffman_tree(vocab: Vocabulary | Sequence[int]) -> HuffmanTree:
+    counts = vocab.counts if isinstance(vocab, Vocabulary) else np.ascontiguousarray(np.asarray(vocab, np.int64))
+    v = int(counts.shape[0])
+    if v == 0:
+        raise RuntimeError("no trainable words")
+    lib = load()
+    steps = C.c_int64()
+    check(lib.cg_build_huffman(ptr(counts, C.c_int64), v, None, None, None, None, C.byref(steps)))
+    off = np.zeros(v + 1, np.int64)
+    nodes = np.zeros(steps.value, np.int32)
+    turns = np.zeros(steps.value, np.uint8)
+    usage = np.zeros(v - 1, np.int64)
+    check(lib.cg_build_huffman(ptr(counts, C.c_int64), v, ptr(off, C.c_int64), ptr(nodes, C.c_int32),
+                               ptr(turns, C.c_uint8), ptr(usage, C.c_int64), C.byref(steps)))
+    return HuffmanTree(off, nodes, turns, usage)
+
+
+class CacheSelection:
+    """huffman.hpp:116-134."""
+
+    def __init__(self, hot: np.ndarray, slot: np.ndarray):
+        self.hot, self.slot = hot, slot
+
+    def size(self) -> int:
+        return int(self.hot.shape[0])
+
+    def hot_nodes(self) -> np.ndarray:
+        return self.hot
+
+    def node_at(self, s: int) -> int:
+        return int(self.hot[s])
+
+    def inner_node_count(self) -> int:
+        return int(self.slot.shape[0])
+
+    def slot_of(self, n: int) -> int:
+        return int(self.slot[n])
+
+
+def select_cached_nodes(tree: HuffmanTree, k: int) -> CacheSelection:
+    if k < 0:
+        raise ValueError("cache node count must be >= 0")
+    inner = tree.inner_count()
+    hot = np.zeros(min(k, inner), np.int32)
+    slot = np.zeros(inner, np.int32)
+    n = load().cg_select_cached_nodes(ptr(tree.usage, C.c_int64), inner, int(k), ptr(hot, C.c_int32),
+                                      ptr(slot, C.c_int32))
+    if n < 0:
+        check(_lib.CG_ERR_INVALID_ARGUMENT)
+    return CacheSelection(hot[:n].copy(), slot)
+
+
+# --------------------------------------------------------------------------- model
+class Model:
+    """model.hpp:25-62: syn0 (V x D) input vectors, syn1 ((V-1) x D) node rows."""
+
+    def __init__(self, vocab_size: int, dim: int, syn0: np.ndarray | None = None, syn1: np.ndarray | None = None):
+        if vocab_size < 2:
+            raise ValueError("model needs a vocabulary of at least two words")
+        if dim < 1:
+            raise ValueError("vector dimension must be >= 1")
+        self.syn0 = syn0 if syn0 is not None else np.zeros((vocab_size, dim), np.float32)
+        self.syn1 = syn1 if syn1 is not None else np.zeros((vocab_size - 1, dim), np.float32)
+
+    def vocab_size(self) -> int:
+        return int(self.syn0.shape[0])
+
+    def dim(self) -> int:
+        return int(self.syn0.shape[1])
+
+    def input_vector(self, w: int) -> np.ndarray:
+        return self.syn0[w]
+
+    def node_weight(self, n: int) -> np.ndarray:
+        return self.syn1[n]
+
+    def input_matrix(self) -> np.ndarray:
+        return self.syn0.reshape(-1)
+
+    def weight_matrix(self) -> np.ndarray:
+        return self.syn1.reshape(-1)
+
+    def copy(self) -> "Model":
+        return Model(self.vocab_size(), self.dim(), self.syn0.copy(), self.syn1.copy())
+
+
+def init_model(vocab_size: int, dim: int, seed: int) -> Model:
+    """model.hpp:66-72, bit-identical."""
+    m = Model(vocab_size, dim)
+    check(load().cg_init_model(vocab_size, dim, seed & 0xFFFFFFFFFFFFFFFF, ptr(m.syn0, C.c_float)))
+    return m
+
+
+def model_desc(vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelection, keep: list) -> CgModelDesc:
+    """Builds the C-ABI view; `keep` holds references so the arrays outlive the call."""
+    counts = np.ascontiguousarray(vocab.counts, np.int64)
+    hot = np.ascontiguousarray(selection.hot, np.int32)
+    keep.extend([counts, hot, tree])
+    d = CgModelDesc()
+    d.vocab_size = vocab.size()
+    d.counts = ptr(counts, C.c_int64)
+    d.total_tokens = vocab.total_tokens()
+    d.path_offsets = ptr(tree.offsets, C.c_int64)
+    d.path_nodes = ptr(tree.nodes, C.c_int32)
+    d.path_turns = ptr(tree.turns, C.c_uint8)
+    d.node_usage = ptr(tree.usage, C.c_int64)
+    d.hot_nodes = ptr(hot, C.c_int32) if hot.size else None
+    d.hot_count = selection.size()
+    return d
+
+
+def _check_consistency(vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelection) -> None:
+    # trainer.hpp:256-260
+    if vocab.size() != tree.leaf_count():
+        raise ValueError("vocabulary and tree sizes disagree")
+    if selection.inner_node_count() != tree.inner_count():
+        raise ValueError("cache selection was built from a different tree")
+
+
+# --------------------------------------------------------------------------- kernel-level API
+class NodeCache:
+    """trainer.hpp:75-138; state on the host, arithmetic (train_center/flush) on the GPU."""
+
+    def __init__(self, selection: CacheSelection, dim: int, flush_interval: int):
+        self.selection, self.dim, self.flush_interval = selection, dim, flush_interval
+        k = max(selection.size(), 0)
+        self.work = np.zeros((max(k, 1), dim), np.float32)
+        self.snap = np.zeros((max(k, 1), dim), np.float32)
+        self.flag = np.zeros(max(k, 1), np.uint8)
+        self._since = 0
+
+    def is_cached(self, slot: int) -> bool:
+        return bool(self.flag[slot])
+
+    def words_since_flush(self) -> int:
+        return self._since
+
+    def row(self, slot: int) -> np.ndarray:
+        return self.work[slot]
+
+    def original(self, slot: int) -> np.ndarray:
+        return self.snap[slot]
+
+    def acquire(self, slot: int, shared_row: np.ndarray) -> np.ndarray:
+        if not self.flag[slot]:
+            self.work[slot] = shared_row
+            self.snap[slot] = shared_row
+            self.flag[slot] = 1
+        return self.work[slot]
+
+    def flush(self, model: Model) -> None:
+        if self.selection.size() > 0:
+            check(load().cg_cache_flush(model.vocab_size(), self.dim, ptr(model.syn1, C.c_float),
+                                        ptr(self.selection.hot, C.c_int32), self.selection.size(),
+                                        ptr(self.work, C.c_float), ptr(self.snap, C.c_float),
+                                        ptr(self.flag, C.c_uint8)))
+        self._since = 0
+
+    def note_center_trained(self) -> bool:
+        self._since += 1
+        return self._since >= self.flush_interval
+
+
+def train_center(center: int, sentence: Sequence[int], center_pos: int, half_window: int, model: Model,
+                 tree: HuffmanTree, selection: CacheSelection, cache: NodeCache, alpha: float,
+                 sigmoid: str | float = "table") -> int:
+    """trainer.hpp:147-175 on the device. sigmoid: "table", "exact" or a constant.
+    Returns the number of sigmoid evaluations (= pairs x path length)."""
+    if isinstance(sigmoid, str):
+        mode, const = {"table": 0, "exact": 1}[sigmoid], 0.0
+    else:
+        mode, const = 2, float(sigmoid)
+    sent = np.ascontiguousarray(np.asarray(sentence, np.int32))
+    slot = np.ascontiguousarray(selection.slot, np.int32)
+    calls = C.c_int64()
+    check(load().cg_train_center(
+        int(center), ptr(sent, C.c_int32), sent.size, int(center_pos), int(half_window), model.vocab_size(),
+        model.dim(), ptr(model.syn0, C.c_float), ptr(model.syn1, C.c_float), ptr(tree.offsets, C.c_int64),
+        ptr(tree.nodes, C.c_int32), ptr(tree.turns, C.c_uint8), ptr(slot, C.c_int32) if selection.size() else None,
+        selection.size(), ptr(cache.work, C.c_float), ptr(cache.snap, C.c_float), ptr(cache.flag, C.c_uint8),
+        float(alpha), mode, const, C.byref(calls)))
+    return calls.value
+
+
+# --------------------------------------------------------------------------- train()
+def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelection, config: TrainConfig,
+          stats: TrainStats | None = None) -> Model:
+    """cachegram::train (trainer.hpp:254-316) on the GPU.
+
+    ``corpus`` is a corpus file path (read with the library's tokenizer) or an
+    in-vocabulary int32 id stream."""
+    config.validate()
+    _check_consistency(vocab, tree, selection)
+    if config.mode == "deterministic" and config.workers != 1:
+        raise ValueError("deterministic mode replays the single-worker stream: set workers = 1")
+    if isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__"):
+        ids = read_id_stream(str(corpus), vocab)
+    else:
+        ids = np.ascontiguousarray(np.asarray(corpus, np.int32))
+    keep: list = []
+    desc = model_desc(vocab, tree, selection, keep)
+    cfg = config.to_c()
+    m = Model(vocab.size(), config.dim)
+    st = CgTrainStats()
+    check(load().cg_train(C.byref(cfg), MODES[config.mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
+                          ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
+    if stats is not None:
+        stats.words_processed = st.words_processed
+        stats.wall_seconds = st.wall_seconds
+        stats.words_per_second = st.words_per_second
+        stats.kernel_seconds = st.kernel_seconds
+        stats.centers, stats.pairs, stats.steps = st.centers, st.pairs, st.steps
+    return m
+
+
+# --------------------------------------------------------------------------- sessions
+class Session:
+    """Device-resident training state (cg_session_*): tree, keep table, ids and model
+    stay in HBM across passes; used by bench.py and the multi-GPU replica driver."""
+
+    def __init__(self, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelection, config: TrainConfig,
+                 device: int = 0, stream: int | None = None):
+        config.validate()
+        _check_consistency(vocab, tree, selection)
+        self._keep: list = []
+        self.config = config
+        self.vocab_size = vocab.size()
+        desc = model_desc(vocab, tree, selection, self._keep)
+        cfg = config.to_c()
+        self._h = C.c_void_p()
+        check(load().cg_session_create(C.byref(cfg), MODES[config.mode], C.byref(desc), device,
+                                       C.c_void_p(stream) if stream else None, C.byref(self._h)))
+        self.n_ids = 0
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            load().cg_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def upload_ids(self, ids: np.ndarray) -> None:
+        ids = np.ascontiguousarray(ids, np.int32)
+        check(load().cg_session_upload_ids(self._h, ptr(ids, C.c_int32), ids.size))
+        self.n_ids = int(ids.size)
+
+    def reset_model(self) -> None:
+        check(load().cg_session_reset_model(self._h))
+
+    def set_model(self, model: Model) -> None:
+        check(load().cg_session_set_model(self._h, ptr(np.ascontiguousarray(model.syn0), C.c_float),
+                                          ptr(np.ascontiguousarray(model.syn1), C.c_float)))
+
+    def tune(self, warps: int = 0, centers_per_warp: int = 0, cache_rows: int = -1) -> None:
+        check(load().cg_session_tune(self._h, warps, centers_per_warp, cache_rows))
+
+    def train_range(self, epoch: int, begin: int, end: int, progress_base: int = 0,
+                    progress_mult: int = 1) -> CgEpochStats:
+        st = CgEpochStats()
+        check(load().cg_session_train_range(self._h, epoch, begin, end, progress_base, progress_mult,
+                                            C.byref(st)))
+        return st
+
+    def train(self) -> TrainStats:
+        st = CgTrainStats()
+        check(load().cg_session_train(self._h, C.byref(st)))
+        return TrainStats(st.words_processed, st.wall_seconds, st.words_per_second, st.kernel_seconds,
+                          st.centers, st.pairs, st.steps)
+
+    def download(self, dim: int | None = None) -> Model:
+        d = dim or self.config.dim
+        m = Model(self.vocab_size, d)
+        check(load().cg_session_download(self._h, ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float)))
+        return m
+
+    def model_buffer(self) -> tuple[int, int, int]:
+        p, n, s = C.c_void_p(), C.c_size_t(), C.c_int32()
+        check(load().cg_session_model_buffer(self._h, C.byref(p), C.byref(n), C.byref(s)))
+        return int(p.value or 0), int(n.value), int(s.value)
+
+    def model_tensor(self):
+        """Zero-copy torch view of the device model buffer (for all-reduce)."""
+        import torch
+
+        p, n, _ = self.model_buffer()
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (n // 4,), "typestr": "<f4", "data": (p, False), "version": 3}
+
+        return torch.as_tensor(_Cai(), device="cuda")

@@ -1,0 +1,808 @@
+// cg_capi.cu -- implementation of the C-ABI declared in include/cachegram_b200.h.
+//
+// Host side of the path (validation, Huffman/selection/keep-prob precompute, device
+// layout, launch sequencing, error mapping) in C++; every training computation is a
+// CUDA kernel (cg_det.cu, cg_hogwild.cu). There is no CPU training fallback.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "cachegram/corpus.hpp"
+#include "cachegram/huffman.hpp"
+#include "cachegram/model.hpp"
+#include "cachegram/trainer.hpp"
+#include "cachegram_b200.h"
+#include "cg_device.cuh"
+#include "cg_kernels.h"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CgError : std::runtime_error {
+    int code;
+    CgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CgError(CG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CG_CUDA(call) check_cuda((call), #call)
+
+[[noreturn]] void invalid(const std::string& m) { throw CgError(CG_ERR_INVALID_ARGUMENT, m); }
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return CG_OK;
+    } catch (const CgError& e) {
+        g_error = e.what();
+        return e.code;
+    } catch (const cachegram::IoError& e) {
+        g_error = e.what();
+        return CG_ERR_IO;
+    } catch (const cachegram::NoTrainableWords& e) {
+        g_error = e.what();
+        return CG_ERR_NO_TRAINABLE_WORDS;
+    } catch (const std::invalid_argument& e) {
+        g_error = e.what();
+        return CG_ERR_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc&) {
+        g_error = "host allocation failed";
+        return CG_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return CG_ERR_INTERNAL;
+    }
+}
+
+// TrainConfig::validate (trainer.hpp:37-47), same messages.
+void validate_config(const cg_config& c) {
+    if (c.dim < 1) invalid("dim must be >= 1");
+    if (c.window < 1) invalid("window must be >= 1");
+    if (c.min_count < 1) invalid("min-count must be >= 1");
+    if (c.sample < 0.0) invalid("sample must be >= 0");
+    if (!(c.alpha0 > 0.0f)) invalid("alpha must be > 0");
+    if (c.iterations < 1) invalid("iterations must be >= 1");
+    if (c.workers < 1) invalid("workers must be >= 1");
+    if (c.cache_nodes < 0) invalid("cache-nodes must be >= 0");
+    if (c.flush_interval < 1) invalid("flush-interval must be >= 1");
+}
+
+void validate_model(const cg_model_desc& m) {
+    if (m.vocab_size < 2) invalid("vocabulary and tree sizes disagree");
+    if (!m.counts || !m.path_offsets || !m.path_nodes || !m.path_turns) invalid("model description has null arrays");
+    if (m.hot_count < 0 || m.hot_count > m.vocab_size - 1)
+        invalid("cache selection was built from a different tree");
+    if (m.hot_count > 0 && !m.hot_nodes) invalid("cache selection was built from a different tree");
+    if (m.path_offsets[0] != 0) invalid("path offsets must start at 0");
+    for (int32_t w = 0; w < m.vocab_size; ++w)
+        if (m.path_offsets[w + 1] <= m.path_offsets[w]) invalid("every word needs a non-empty tree path");
+    const int64_t steps = m.path_offsets[m.vocab_size];
+    for (int64_t k = 0; k < steps; ++k)
+        if (m.path_nodes[k] < 0 || m.path_nodes[k] >= m.vocab_size - 1 || m.path_turns[k] > 1)
+            invalid("vocabulary and tree sizes disagree");
+    for (int32_t s = 0; s < m.hot_count; ++s)
+        if (m.hot_nodes[s] < 0 || m.hot_nodes[s] >= m.vocab_size - 1)
+            invalid("cache selection was built from a different tree");
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    void alloc(size_t count) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = count;
+        if (count) CG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void upload(const T* host, size_t count, cudaStream_t s) {
+        alloc(count);
+        if (count) CG_CUDA(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+// ---- small device helpers of the layout --------------------------------------
+__global__ void init_syn0_kernel(float* out, int64_t rows, int32_t dim, int32_t stride, uint64_t key, float inv_dim) {
+    // model.hpp:66-72: value i (row-major, unpadded) = (unit24(draw i) - 0.5f) * (1/D)
+    const int64_t n = rows * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dim, d = i - r * dim;
+        const float u = cgdev::unit24(cgdev::ctr_draw(key, static_cast<uint64_t>(i)));
+        out[r * stride + d] = __fmul_rn(__fsub_rn(u, 0.5f), inv_dim);
+    }
+}
+
+// dst[r*ds + d] = src[perm(r)*ss + d]; perm == nullptr means identity. Pads are left alone.
+__global__ void gather_rows_kernel(float* dst, int32_t ds, const float* src, int32_t ss, const int32_t* perm,
+                                   int64_t rows, int32_t dim) {
+    const int64_t n = rows * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dim, d = i - r * dim;
+        const int64_t sr = perm ? perm[r] : r;
+        dst[r * ds + d] = src[sr * ss + d];
+    }
+}
+// dst[perm(r)*ds + d] = src[r*ss + d]
+__global__ void scatter_rows_kernel(float* dst, int32_t ds, const float* src, int32_t ss, const int32_t* perm,
+                                    int64_t rows, int32_t dim) {
+    const int64_t n = rows * dim;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / dim, d = i - r * dim;
+        const int64_t dr = perm ? perm[r] : r;
+        dst[dr * ds + d] = src[r * ss + d];
+    }
+}
+
+unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+}  // namespace
+
+// ============================================================================ session
+struct cg_session {
+    cg_config cfg{};
+    int32_t mode = CG_MODE_HOGWILD;
+    int32_t device = 0;
+    cudaStream_t stream = nullptr;
+    int32_t V = 0, D = 0, Dp = 0, K = 0;
+    int64_t total_tokens = 0;
+    int32_t max_depth = 0;
+
+    // host layout maps (hogwild): node id -> device row and back
+    std::vector<int32_t> row_of_node, node_of_row;
+
+    DevBuf<float> model;  // det: syn0[V*D] syn1[(V-1)*D]; hogwild: padded, permuted
+    DevBuf<float> sigmoid, keep, stage;
+    DevBuf<int32_t> ids, node_of_row_dev, row_of_node_dev;
+    int64_t n_ids = 0;
+
+    // det mode
+    DevBuf<int64_t> det_off;
+    DevBuf<int32_t> det_node, det_slot, det_hot, det_acq;
+    DevBuf<uint8_t> det_turn, det_flag;
+    DevBuf<float> det_work, det_snap;
+    DevBuf<cgk::DetState> det_state;
+
+    // hogwild mode
+    DevBuf<int32_t> hw_off, hw_code, kept;
+    DevBuf<float> sent_alpha;
+    DevBuf<uint32_t> tile_count;
+    DevBuf<uint64_t> tile_off;
+    DevBuf<unsigned long long> counters;
+    int tune_warps = 0, tune_cpw = 0, tune_rows = -1;
+
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+
+    float* syn0() const { return model.p; }
+    float* syn1() const { return model.p + static_cast<size_t>(V) * (mode == CG_MODE_DETERMINISTIC ? D : Dp); }
+    int32_t stride() const { return mode == CG_MODE_DETERMINISTIC ? D : Dp; }
+
+    ~cg_session() {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+float host_sig_scale() { return static_cast<float>(1000) / (2.0f * 6.0f); }
+
+cgk::DetModel det_model(const cg_session& s) {
+    cgk::DetModel m{};
+    m.syn0 = s.syn0();
+    m.syn1 = s.syn1();
+    m.dim = s.D;
+    m.vocab = s.V;
+    m.path_off = s.det_off.p;
+    m.path_node = s.det_node.p;
+    m.path_turn = s.det_turn.p;
+    m.slot_of = s.K > 0 ? s.det_slot.p : nullptr;
+    m.hot_nodes = s.det_hot.p;
+    m.hot_count = s.K;
+    m.cache_work = s.det_work.p;
+    m.cache_snap = s.det_snap.p;
+    m.cache_flag = s.det_flag.p;
+    m.acquired = s.det_acq.p;
+    m.sigmoid = s.sigmoid.p;
+    m.sig_scale = host_sig_scale();
+    return m;
+}
+
+void session_reset_model(cg_session& s) {
+    const uint64_t key = cachegram::mix_seed(s.cfg.seed, 0x1817);
+    const int32_t st = s.stride();
+    CG_CUDA(cudaMemsetAsync(s.model.p, 0, s.model.n * sizeof(float), s.stream));
+    const int64_t n = static_cast<int64_t>(s.V) * s.D;
+    init_syn0_kernel<<<grid_for(n), 256, 0, s.stream>>>(s.syn0(), s.V, s.D, st, key, 1.0f / static_cast<float>(s.D));
+    CG_CUDA(cudaGetLastError());
+    if (s.mode == CG_MODE_DETERMINISTIC) {
+        cgk::DetState init{};
+        init.rng = cachegram::mix_seed(s.cfg.seed, 0);  // trainer.hpp:203, worker 0
+        init.alpha = cachegram::update_alpha_host(0, 0, s.cfg.alpha0);
+        CG_CUDA(cudaMemcpyAsync(s.det_state.p, &init, sizeof init, cudaMemcpyHostToDevice, s.stream));
+        if (s.K > 0) CG_CUDA(cudaMemsetAsync(s.det_flag.p, 0, s.det_flag.n, s.stream));
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int cg_abi_version(void) { return CG_ABI_VERSION; }
+const char* cg_last_error(void) { return g_error.c_str(); }
+
+int cg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+double cg_keep_probability(int64_t count, int64_t total_tokens, double sample) {
+    return cachegram::keep_probability(count, total_tokens, sample);
+}
+
+float cg_update_alpha(uint64_t words_processed, uint64_t total_words, float alpha0) {
+    return cachegram::update_alpha_host(words_processed, total_words, alpha0);
+}
+
+void cg_sigmoid_table(float* out) {
+    const cachegram::SigmoidTable t;
+    std::memcpy(out, t.data(), 1000 * sizeof(float));
+}
+
+int cg_init_model(int32_t vocab_size, int32_t dim, uint64_t seed, float* syn0) {
+    return guarded([&] {
+        if (vocab_size < 2) invalid("model needs a vocabulary of at least two words");
+        if (dim < 1) invalid("vector dimension must be >= 1");
+        cachegram::init_model_into(vocab_size, dim, seed, syn0);
+    });
+}
+
+int cg_build_huffman(const int64_t* counts, int32_t vocab_size, int64_t* path_offsets, int32_t* path_nodes,
+                     uint8_t* path_turns, int64_t* node_usage, int64_t* n_steps) {
+    return guarded([&] {
+        const cachegram::HuffmanTree t = cachegram::huffman_from_counts(counts, vocab_size);
+        if (n_steps) *n_steps = static_cast<int64_t>(t.steps().size());
+        if (path_offsets)
+            for (size_t i = 0; i < t.offsets().size(); ++i) path_offsets[i] = static_cast<int64_t>(t.offsets()[i]);
+        if (path_nodes)
+            for (size_t k = 0; k < t.steps().size(); ++k) {
+                path_nodes[k] = t.steps()[k].node;
+                path_turns[k] = t.steps()[k].turn;
+            }
+        if (node_usage)
+            for (int32_t n = 0; n < t.inner_count(); ++n) node_usage[n] = t.node_usage(n);
+    });
+}
+
+int32_t cg_select_cached_nodes(const int64_t* node_usage, int32_t inner_count, int32_t k, int32_t* hot_nodes,
+                               int32_t* slot_of) {
+    int32_t size = -1;
+    const int rc = guarded([&] {
+        if (k < 0) invalid("cache node count must be >= 0");
+        std::vector<int32_t> order(static_cast<size_t>(inner_count));
+        for (int32_t i = 0; i < inner_count; ++i) order[static_cast<size_t>(i)] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [node_usage](int32_t a, int32_t b) { return node_usage[a] > node_usage[b]; });
+        size = std::min(k, inner_count);
+        for (int32_t i = 0; i < inner_count; ++i) slot_of[i] = -1;
+        for (int32_t s = 0; s < size; ++s) {
+            hot_nodes[s] = order[static_cast<size_t>(s)];
+            slot_of[order[static_cast<size_t>(s)]] = s;
+        }
+    });
+    return rc == CG_OK ? size : -1;
+}
+
+// ---- corpus -------------------------------------------------------------------
+}  // extern "C"
+
+struct cg_corpus {
+    cachegram::Vocabulary vocab;
+};
+
+extern "C" {
+
+int cg_corpus_open(const char* path, int64_t min_count, cg_corpus** out) {
+    return guarded([&] {
+        if (min_count < 1) invalid("min-count must be >= 1");
+        *out = new cg_corpus{cachegram::build_vocabulary_file(path, min_count)};
+    });
+}
+int32_t cg_corpus_vocab_size(const cg_corpus* c) { return c->vocab.size(); }
+int64_t cg_corpus_total_tokens(const cg_corpus* c) { return c->vocab.total_tokens(); }
+int64_t cg_corpus_word_bytes(const cg_corpus* c) {
+    int64_t n = 0;
+    for (int32_t i = 0; i < c->vocab.size(); ++i) n += static_cast<int64_t>(c->vocab.word(i).size()) + 1;
+    return n;
+}
+int cg_corpus_export_vocab(const cg_corpus* c, int64_t* counts, char* words) {
+    return guarded([&] {
+        for (int32_t i = 0; i < c->vocab.size(); ++i) {
+            if (counts) counts[i] = c->vocab.count(i);
+            if (words) {
+                const std::string& w = c->vocab.word(i);
+                std::memcpy(words, w.data(), w.size());
+                words += w.size();
+                *words++ = '\0';
+            }
+        }
+    });
+}
+int cg_corpus_read_ids(const cg_corpus* c, const char* path, int32_t* ids, int64_t capacity, int64_t* n_ids) {
+    return guarded([&] {
+        const std::vector<int32_t> v = cachegram::read_id_stream(path, c->vocab);
+        if (n_ids) *n_ids = static_cast<int64_t>(v.size());
+        if (ids) {
+            if (static_cast<int64_t>(v.size()) > capacity) invalid("id buffer too small");
+            std::memcpy(ids, v.data(), v.size() * sizeof(int32_t));
+        }
+    });
+}
+void cg_corpus_close(cg_corpus* c) { delete c; }
+
+// ---- sessions -------------------------------------------------------------------
+int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* md, int32_t device, void* stream,
+                      cg_session** out) {
+    *out = nullptr;
+    auto s = std::make_unique<cg_session>();
+    const int rc = guarded([&] {
+        if (!cfg || !md) invalid("null config or model");
+        validate_config(*cfg);
+        validate_model(*md);
+        if (mode != CG_MODE_HOGWILD && mode != CG_MODE_DETERMINISTIC) invalid("unknown training mode");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+        }
+        if (device < 0 || device >= ndev) invalid("device ordinal out of range");
+        CG_CUDA(cudaSetDevice(device));
+        s->cfg = *cfg;
+        s->mode = mode;
+        s->device = device;
+        s->stream = static_cast<cudaStream_t>(stream);
+        s->V = md->vocab_size;
+        s->D = cfg->dim;
+        s->Dp = (cfg->dim + 3) / 4 * 4;
+        s->K = md->hot_count;
+        s->total_tokens = md->total_tokens;
+        const int32_t V = s->V;
+        const int64_t steps = md->path_offsets[V];
+        for (int32_t w = 0; w < V; ++w)
+            s->max_depth = std::max<int32_t>(s->max_depth, static_cast<int32_t>(md->path_offsets[w + 1] - md->path_offsets[w]));
+        for (auto& e : s->ev) CG_CUDA(cudaEventCreate(&e));
+
+        const cachegram::SigmoidTable table;
+        s->sigmoid.upload(table.data(), 1000, s->stream);
+        if (cfg->sample > 0.0) {
+            std::vector<float> kp(static_cast<size_t>(V));
+            for (int32_t w = 0; w < V; ++w)
+                kp[static_cast<size_t>(w)] =
+                    static_cast<float>(cachegram::keep_probability(md->counts[w], md->total_tokens, cfg->sample));
+            s->keep.upload(kp.data(), kp.size(), s->stream);
+        }
+
+        if (mode == CG_MODE_DETERMINISTIC) {
+            s->model.alloc(static_cast<size_t>(V) * s->D + static_cast<size_t>(V - 1) * s->D);
+            s->det_off.upload(md->path_offsets, static_cast<size_t>(V) + 1, s->stream);
+            s->det_node.upload(md->path_nodes, static_cast<size_t>(steps), s->stream);
+            s->det_turn.upload(md->path_turns, static_cast<size_t>(steps), s->stream);
+            if (s->K > 0) {
+                std::vector<int32_t> slot(static_cast<size_t>(V - 1), -1);
+                for (int32_t k = 0; k < s->K; ++k) slot[static_cast<size_t>(md->hot_nodes[k])] = k;
+                s->det_slot.upload(slot.data(), slot.size(), s->stream);
+                s->det_hot.upload(md->hot_nodes, static_cast<size_t>(s->K), s->stream);
+                s->det_work.alloc(static_cast<size_t>(s->K) * s->D);
+                s->det_snap.alloc(static_cast<size_t>(s->K) * s->D);
+                s->det_flag.alloc(static_cast<size_t>(s->K));
+                s->det_acq.alloc(static_cast<size_t>(s->K));
+            }
+            s->det_state.alloc(1);
+        } else {
+            if (s->Dp > 4 * 96) invalid("hogwild mode supports dim <= 384");
+            if (s->max_depth > 64) invalid("hogwild mode supports Huffman depth <= 64");
+            if (steps >= (int64_t{1} << 31)) invalid("tree too large for 32-bit path offsets");
+            // device row order: hot slots first (slot order), then the remaining inner
+            // nodes by (usage desc, id asc); "hot" becomes row < K in the kernel
+            std::vector<int32_t> rest;
+            std::vector<char> is_hot(static_cast<size_t>(V - 1), 0);
+            s->node_of_row.reserve(static_cast<size_t>(V - 1));
+            for (int32_t k = 0; k < s->K; ++k) {
+                s->node_of_row.push_back(md->hot_nodes[k]);
+                is_hot[static_cast<size_t>(md->hot_nodes[k])] = 1;
+            }
+            for (int32_t n = 0; n < V - 1; ++n)
+                if (!is_hot[static_cast<size_t>(n)]) rest.push_back(n);
+            if (md->node_usage)
+                std::stable_sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
+                    return md->node_usage[a] > md->node_usage[b];
+                });
+            s->node_of_row.insert(s->node_of_row.end(), rest.begin(), rest.end());
+            s->row_of_node.assign(static_cast<size_t>(V - 1), 0);
+            for (int32_t r = 0; r < V - 1; ++r) s->row_of_node[static_cast<size_t>(s->node_of_row[static_cast<size_t>(r)])] = r;
+            std::vector<int32_t> off(static_cast<size_t>(V) + 1), code(static_cast<size_t>(steps));
+            for (int32_t w = 0; w <= V; ++w) off[static_cast<size_t>(w)] = static_cast<int32_t>(md->path_offsets[w]);
+            for (int64_t k = 0; k < steps; ++k)
+                code[static_cast<size_t>(k)] = (s->row_of_node[static_cast<size_t>(md->path_nodes[k])] << 1) | md->path_turns[k];
+            s->hw_off.upload(off.data(), off.size(), s->stream);
+            s->hw_code.upload(code.data(), code.size(), s->stream);
+            s->node_of_row_dev.upload(s->node_of_row.data(), s->node_of_row.size(), s->stream);
+            s->row_of_node_dev.upload(s->row_of_node.data(), s->row_of_node.size(), s->stream);
+            s->model.alloc(static_cast<size_t>(V) * s->Dp + static_cast<size_t>(V - 1) * s->Dp);
+            s->counters.alloc(4);
+        }
+        session_reset_model(*s);
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+    if (rc == CG_OK) *out = s.release();
+    return rc;
+}
+
+void cg_session_destroy(cg_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->device);
+    cudaStreamSynchronize(s->stream);
+    delete s;
+}
+
+int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids) {
+    return guarded([&] {
+        if (n_ids < 0) invalid("negative id count");
+        CG_CUDA(cudaSetDevice(s->device));
+        for (int64_t i = 0; i < n_ids; ++i)
+            if (ids[i] < 0 || ids[i] >= s->V) invalid("id out of vocabulary range");
+        s->ids.upload(ids, static_cast<size_t>(n_ids), s->stream);
+        s->n_ids = n_ids;
+        if (s->mode == CG_MODE_HOGWILD) {
+            s->kept.alloc(static_cast<size_t>(std::max<int64_t>(n_ids, 1)));
+            s->sent_alpha.alloc(static_cast<size_t>(n_ids / cgdev::kSentence + 2));
+            const int64_t nt = cgk::sub_tiles(n_ids);
+            s->tile_count.alloc(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+            s->tile_off.alloc(static_cast<size_t>(nt + 1));
+        }
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_reset_model(cg_session* s) {
+    return guarded([&] {
+        CG_CUDA(cudaSetDevice(s->device));
+        session_reset_model(*s);
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_set_model(cg_session* s, const float* syn0, const float* syn1) {
+    return guarded([&] {
+        CG_CUDA(cudaSetDevice(s->device));
+        const size_t n0 = static_cast<size_t>(s->V) * s->D, n1 = static_cast<size_t>(s->V - 1) * s->D;
+        if (s->mode == CG_MODE_DETERMINISTIC) {
+            CG_CUDA(cudaMemcpyAsync(s->syn0(), syn0, n0 * 4, cudaMemcpyHostToDevice, s->stream));
+            CG_CUDA(cudaMemcpyAsync(s->syn1(), syn1, n1 * 4, cudaMemcpyHostToDevice, s->stream));
+        } else {
+            s->stage.alloc(n0 + n1);
+            CG_CUDA(cudaMemcpyAsync(s->stage.p, syn0, n0 * 4, cudaMemcpyHostToDevice, s->stream));
+            CG_CUDA(cudaMemcpyAsync(s->stage.p + n0, syn1, n1 * 4, cudaMemcpyHostToDevice, s->stream));
+            CG_CUDA(cudaMemsetAsync(s->model.p, 0, s->model.n * 4, s->stream));
+            scatter_rows_kernel<<<grid_for(static_cast<int64_t>(n0)), 256, 0, s->stream>>>(s->syn0(), s->Dp, s->stage.p, s->D, nullptr, s->V, s->D);
+            scatter_rows_kernel<<<grid_for(static_cast<int64_t>(n1)), 256, 0, s->stream>>>(s->syn1(), s->Dp, s->stage.p + n0, s->D, s->row_of_node_dev.p, s->V - 1, s->D);
+            CG_CUDA(cudaGetLastError());
+        }
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out) {
+    return guarded([&] {
+        CG_CUDA(cudaSetDevice(s->device));
+        const size_t n0 = static_cast<size_t>(s->V) * s->D, n1 = static_cast<size_t>(s->V - 1) * s->D;
+        if (s->mode == CG_MODE_DETERMINISTIC) {
+            if (syn0_out) CG_CUDA(cudaMemcpyAsync(syn0_out, s->syn0(), n0 * 4, cudaMemcpyDeviceToHost, s->stream));
+            if (syn1_out) CG_CUDA(cudaMemcpyAsync(syn1_out, s->syn1(), n1 * 4, cudaMemcpyDeviceToHost, s->stream));
+        } else {
+            if (s->stage.n < n0 + n1) s->stage.alloc(n0 + n1);
+            gather_rows_kernel<<<grid_for(static_cast<int64_t>(n0)), 256, 0, s->stream>>>(s->stage.p, s->D, s->syn0(), s->Dp, nullptr, s->V, s->D);
+            gather_rows_kernel<<<grid_for(static_cast<int64_t>(n1)), 256, 0, s->stream>>>(s->stage.p + n0, s->D, s->syn1(), s->Dp, s->row_of_node_dev.p, s->V - 1, s->D);
+            CG_CUDA(cudaGetLastError());
+            if (syn0_out) CG_CUDA(cudaMemcpyAsync(syn0_out, s->stage.p, n0 * 4, cudaMemcpyDeviceToHost, s->stream));
+            if (syn1_out) CG_CUDA(cudaMemcpyAsync(syn1_out, s->stage.p + n0, n1 * 4, cudaMemcpyDeviceToHost, s->stream));
+        }
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int32_t* row_stride_floats) {
+    return guarded([&] {
+        if (device_ptr) *device_ptr = s->model.p;
+        if (bytes) *bytes = s->model.n * sizeof(float);
+        if (row_stride_floats) *row_stride_floats = s->stride();
+    });
+}
+
+int cg_session_tune(cg_session* s, int32_t warps_per_block, int32_t centers_per_warp, int32_t smem_cache_rows) {
+    return guarded([&] {
+        s->tune_warps = warps_per_block;
+        s->tune_cpw = centers_per_warp;
+        s->tune_rows = smem_cache_rows;
+    });
+}
+
+int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int64_t tok_end, uint64_t progress_base,
+                           uint32_t progress_mult, cg_epoch_stats* st) {
+    return guarded([&] {
+        CG_CUDA(cudaSetDevice(s->device));
+        if (tok_begin < 0 || tok_end > s->n_ids || tok_begin > tok_end) invalid("token range out of bounds");
+        if (progress_mult < 1) invalid("progress_mult must be >= 1");
+        cg_epoch_stats out{};
+        const int64_t n = tok_end - tok_begin;
+        const uint64_t total_words = static_cast<uint64_t>(s->cfg.iterations) * static_cast<uint64_t>(s->total_tokens);
+        out.words = static_cast<uint64_t>(n);
+        if (s->mode == CG_MODE_DETERMINISTIC) {
+            cgk::DetPass p{};
+            p.ids = s->ids.p + tok_begin;
+            p.n_ids = n;
+            p.keep = s->keep.p;
+            p.window = s->cfg.window;
+            p.flush_interval = s->cfg.flush_interval;
+            p.total_words = total_words;
+            p.alpha0 = s->cfg.alpha0;
+            cgk::DetState before{};
+            CG_CUDA(cudaMemcpyAsync(&before, s->det_state.p, sizeof before, cudaMemcpyDeviceToHost, s->stream));
+            CG_CUDA(cudaEventRecord(s->ev[2], s->stream));
+            cgk::launch_det_pass(det_model(*s), p, s->det_state.p, s->stream);
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaEventRecord(s->ev[3], s->stream));
+            cgk::DetState after{};
+            CG_CUDA(cudaMemcpyAsync(&after, s->det_state.p, sizeof after, cudaMemcpyDeviceToHost, s->stream));
+            CG_CUDA(cudaStreamSynchronize(s->stream));
+            float ms = 0.f;
+            CG_CUDA(cudaEventElapsedTime(&ms, s->ev[2], s->ev[3]));
+            out.train_ms = ms;
+            out.kept = after.centers - before.centers;
+            out.pairs = after.pairs - before.pairs;
+            out.steps = after.steps - before.steps;
+            out.train_launches = 1;
+        } else {
+            cgk::SubArgs a{};
+            a.ids = s->ids.p + tok_begin;
+            a.n = n;
+            a.index_base = tok_begin;
+            a.keep = s->keep.p;
+            a.key = cgdev::mix64(s->cfg.seed ^ 0x5ab5a3b1e5d00d1full) + 0x100000001b3ull * static_cast<uint64_t>(epoch);
+            a.tile_count = s->tile_count.p;
+            a.tile_off = s->tile_off.p;
+            a.kept = s->kept.p;
+            a.sent_alpha = s->sent_alpha.p;
+            a.progress_base = progress_base;
+            a.progress_mult = progress_mult;
+            a.total_words = total_words;
+            a.alpha0 = s->cfg.alpha0;
+            CG_CUDA(cudaEventRecord(s->ev[0], s->stream));
+            int sub_launches = 0;
+            cgk::launch_subsample(a, s->stream, &sub_launches);
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaMemsetAsync(s->counters.p, 0, 4 * sizeof(unsigned long long), s->stream));
+            CG_CUDA(cudaEventRecord(s->ev[1], s->stream));
+            cgk::HogArgs h{};
+            h.syn0 = s->syn0();
+            h.syn1 = s->syn1();
+            h.d4 = s->Dp / 4;
+            h.path_off = s->hw_off.p;
+            h.path_code = s->hw_code.p;
+            h.kept = s->kept.p;
+            h.n_kept_dev = s->tile_off.p + cgk::sub_tiles(n);
+            h.sent_alpha = s->sent_alpha.p;
+            h.sigmoid = s->sigmoid.p;
+            h.sig_scale = host_sig_scale();
+            h.window = s->cfg.window;
+            h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
+            h.counters = s->counters.p;
+            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->K, s->tune_warps, s->tune_cpw, s->tune_rows);
+            CG_CUDA(cudaEventRecord(s->ev[2], s->stream));
+            cgk::launch_hogwild(h, g, s->stream);
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaEventRecord(s->ev[3], s->stream));
+            unsigned long long cnt[4] = {0, 0, 0, 0};
+            uint64_t kept = 0;
+            CG_CUDA(cudaMemcpyAsync(cnt, s->counters.p, sizeof cnt, cudaMemcpyDeviceToHost, s->stream));
+            CG_CUDA(cudaMemcpyAsync(&kept, h.n_kept_dev, sizeof kept, cudaMemcpyDeviceToHost, s->stream));
+            CG_CUDA(cudaStreamSynchronize(s->stream));
+            float sub_ms = 0.f, tr_ms = 0.f;
+            CG_CUDA(cudaEventElapsedTime(&sub_ms, s->ev[0], s->ev[1]));
+            CG_CUDA(cudaEventElapsedTime(&tr_ms, s->ev[2], s->ev[3]));
+            out.subsample_ms = sub_ms;
+            out.train_ms = tr_ms;
+            out.kept = kept;
+            out.pairs = cnt[1];
+            out.steps = cnt[2];
+            out.train_launches = 1;
+            out.other_launches = sub_launches;
+            if (cnt[3] != kept) throw CgError(CG_ERR_INTERNAL, "hogwild kernel did not cover every kept center");
+        }
+        if (st) *st = out;
+    });
+}
+
+int cg_session_train(cg_session* s, cg_train_stats* st) {
+    return guarded([&] {
+        cg_train_stats out{};
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int32_t it = 0; it < s->cfg.iterations; ++it) {
+            cg_epoch_stats e{};
+            const int rc = cg_session_train_range(s, it, 0, s->n_ids,
+                                                  static_cast<uint64_t>(it) * static_cast<uint64_t>(s->n_ids), 1, &e);
+            if (rc != CG_OK) throw CgError(rc, g_error);
+            out.kernel_seconds += (e.train_ms + e.subsample_ms) * 1e-3;
+            out.centers += e.kept;
+            out.pairs += e.pairs;
+            out.steps += e.steps;
+            out.words_processed += e.words;
+        }
+        out.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out.words_per_second = out.wall_seconds > 0 ? static_cast<double>(out.words_processed) / out.wall_seconds : 0.0;
+        if (st) *st = out;
+    });
+}
+
+int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids, int64_t n_ids,
+             float* syn0_out, float* syn1_out, cg_train_stats* stats) {
+    cg_session* s = nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    int rc = cg_session_create(cfg, mode, model, dev, nullptr, &s);
+    if (rc != CG_OK) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    rc = cg_session_upload_ids(s, ids, n_ids);
+    cg_train_stats st{};
+    if (rc == CG_OK) rc = cg_session_train(s, &st);
+    if (rc == CG_OK) rc = cg_session_download(s, syn0_out, syn1_out);
+    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    st.words_per_second = st.wall_seconds > 0 ? static_cast<double>(st.words_processed) / st.wall_seconds : 0.0;
+    if (stats) *stats = st;
+    cg_session_destroy(s);
+    return rc;
+}
+
+// ---- kernel-level entries ---------------------------------------------------------
+int cg_train_center(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
+                    int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
+                    const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
+                    const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
+                    uint8_t* cache_flag, float alpha, int32_t sigmoid_mode, float sig_const, int64_t* sigmoid_calls) {
+    return guarded([&] {
+        if (vocab_size < 2 || dim < 1) invalid("bad model geometry");
+        if (center < 0 || center >= vocab_size) invalid("center out of range");
+        if (center_pos < 0 || center_pos >= sentence_len) invalid("center position out of range");
+        if (half_window < 0) invalid("half window must be >= 0");
+        if (hot_count > 0 && (!slot_of || !cache_work || !cache_snap || !cache_flag)) invalid("cache arrays missing");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+        }
+        cudaStream_t st = nullptr;
+        const size_t n0 = static_cast<size_t>(vocab_size) * dim, n1 = static_cast<size_t>(vocab_size - 1) * dim;
+        const int64_t steps = path_offsets[vocab_size];
+        DevBuf<float> d0, d1, work, snap, sig;
+        DevBuf<int64_t> off;
+        DevBuf<int32_t> node, slot, sent, acq, nacq;
+        DevBuf<uint8_t> turn, flag;
+        DevBuf<unsigned long long> evals;
+        d0.upload(syn0, n0, st);
+        d1.upload(syn1, n1, st);
+        off.upload(path_offsets, static_cast<size_t>(vocab_size) + 1, st);
+        node.upload(path_nodes, static_cast<size_t>(steps), st);
+        turn.upload(path_turns, static_cast<size_t>(steps), st);
+        sent.upload(sentence, static_cast<size_t>(sentence_len), st);
+        const cachegram::SigmoidTable table;
+        sig.upload(table.data(), 1000, st);
+        int32_t zero = 0;
+        nacq.upload(&zero, 1, st);
+        evals.alloc(1);
+        cgk::DetModel m{};
+        m.syn0 = d0.p;
+        m.syn1 = d1.p;
+        m.dim = dim;
+        m.vocab = vocab_size;
+        m.path_off = off.p;
+        m.path_node = node.p;
+        m.path_turn = turn.p;
+        m.sigmoid = sig.p;
+        m.sig_scale = host_sig_scale();
+        if (hot_count > 0) {
+            slot.upload(slot_of, static_cast<size_t>(vocab_size - 1), st);
+            work.upload(cache_work, static_cast<size_t>(hot_count) * dim, st);
+            snap.upload(cache_snap, static_cast<size_t>(hot_count) * dim, st);
+            flag.upload(cache_flag, static_cast<size_t>(hot_count), st);
+            acq.alloc(static_cast<size_t>(hot_count));
+            m.slot_of = slot.p;
+            m.hot_count = hot_count;
+            m.cache_work = work.p;
+            m.cache_snap = snap.p;
+            m.cache_flag = flag.p;
+            m.acquired = acq.p;
+        }
+        cgk::DetCenter c{};
+        c.center = center;
+        c.sentence = sent.p;
+        c.len = sentence_len;
+        c.pos = center_pos;
+        c.half_window = half_window;
+        c.alpha = alpha;
+        c.sigmoid_mode = sigmoid_mode;
+        c.sig_const = sig_const;
+        c.n_acquired = nacq.p;
+        c.evals = evals.p;
+        cgk::launch_det_center(m, c, st);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpy(syn0, d0.p, n0 * 4, cudaMemcpyDeviceToHost));
+        CG_CUDA(cudaMemcpy(syn1, d1.p, n1 * 4, cudaMemcpyDeviceToHost));
+        if (hot_count > 0) {
+            CG_CUDA(cudaMemcpy(cache_work, work.p, static_cast<size_t>(hot_count) * dim * 4, cudaMemcpyDeviceToHost));
+            CG_CUDA(cudaMemcpy(cache_snap, snap.p, static_cast<size_t>(hot_count) * dim * 4, cudaMemcpyDeviceToHost));
+            CG_CUDA(cudaMemcpy(cache_flag, flag.p, static_cast<size_t>(hot_count), cudaMemcpyDeviceToHost));
+        }
+        unsigned long long e = 0;
+        CG_CUDA(cudaMemcpy(&e, evals.p, sizeof e, cudaMemcpyDeviceToHost));
+        if (sigmoid_calls) *sigmoid_calls = static_cast<int64_t>(e);
+    });
+}
+
+int cg_cache_flush(int32_t vocab_size, int32_t dim, float* syn1, const int32_t* hot_nodes, int32_t hot_count,
+                   float* cache_work, const float* cache_snap, uint8_t* cache_flag) {
+    return guarded([&] {
+        if (hot_count <= 0) return;
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+            cudaGetLastError();
+            throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+        }
+        const size_t n1 = static_cast<size_t>(vocab_size - 1) * dim;
+        DevBuf<float> d1, work, snap;
+        DevBuf<int32_t> hot;
+        DevBuf<uint8_t> flag;
+        d1.upload(syn1, n1, nullptr);
+        work.upload(cache_work, static_cast<size_t>(hot_count) * dim, nullptr);
+        snap.upload(cache_snap, static_cast<size_t>(hot_count) * dim, nullptr);
+        flag.upload(cache_flag, static_cast<size_t>(hot_count), nullptr);
+        hot.upload(hot_nodes, static_cast<size_t>(hot_count), nullptr);
+        cgk::DetModel m{};
+        m.syn1 = d1.p;
+        m.dim = dim;
+        m.vocab = vocab_size;
+        m.hot_nodes = hot.p;
+        m.hot_count = hot_count;
+        m.cache_work = work.p;
+        m.cache_snap = snap.p;
+        m.cache_flag = flag.p;
+        cgk::launch_det_flush_flags(m, nullptr);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpy(syn1, d1.p, n1 * 4, cudaMemcpyDeviceToHost));
+        CG_CUDA(cudaMemcpy(cache_flag, flag.p, static_cast<size_t>(hot_count), cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"

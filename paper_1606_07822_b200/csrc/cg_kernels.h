@@ -1,0 +1,121 @@
+// cg_kernels.h -- host-side launchers of the sm_100a kernels (internal to the .so).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cgk {
+
+// ---------------- deterministic single-stream mode (K2) ----------------------
+// Reference layout: syn0 [V*D], syn1 [(V-1)*D] in reference node-id order.
+struct DetModel {
+    float* syn0;
+    float* syn1;
+    int32_t dim;
+    int32_t vocab;
+    const int64_t* path_off;   // [V+1]
+    const int32_t* path_node;  // reference node ids
+    const uint8_t* path_turn;
+    const int32_t* slot_of;    // [V-1] or nullptr (no cache)
+    const int32_t* hot_nodes;  // [K]
+    int32_t hot_count;
+    float* cache_work;         // [K*D]
+    float* cache_snap;         // [K*D]
+    uint8_t* cache_flag;       // [K]
+    int32_t* acquired;         // [K] acquire order
+    const float* sigmoid;      // [1000]
+    float sig_scale;           // (float)1000 / 12.0f, folded on the host
+};
+
+// Worker state that carries across passes (trainer.hpp:203-212).
+struct DetState {
+    uint64_t rng;
+    uint64_t progress;    // ProgressCounter::words_processed
+    uint64_t unreported;
+    float alpha;
+    int32_t since_flush;
+    int32_t n_acquired;
+    int32_t pad;
+    uint64_t centers, pairs, steps, words;
+};
+
+struct DetPass {
+    const int32_t* ids;
+    int64_t n_ids;
+    const float* keep;     // [V] or nullptr when sample == 0
+    int32_t window;
+    int32_t flush_interval;
+    uint64_t total_words;  // iterations * total_tokens
+    float alpha0;
+};
+
+void launch_det_pass(const DetModel& m, const DetPass& p, DetState* state, cudaStream_t s);
+
+struct DetCenter {
+    int32_t center;
+    const int32_t* sentence;
+    int64_t len;
+    int64_t pos;
+    int32_t half_window;
+    float alpha;
+    int32_t sigmoid_mode;  // 0 table, 1 exact, 2 constant
+    float sig_const;
+    int32_t* n_acquired;   // device scalar
+    unsigned long long* evals;
+};
+void launch_det_center(const DetModel& m, const DetCenter& c, cudaStream_t s);
+void launch_det_flush_flags(const DetModel& m, cudaStream_t s);
+
+// ---------------- throughput mode: subsampling + pair generation (K3) ---------
+constexpr int kSubTile = 2048;  // tokens per subsampling block (256 threads x 8)
+
+struct SubArgs {
+    const int32_t* ids;   // range start
+    int64_t n;            // tokens in the range
+    int64_t index_base;   // global index of ids[0] (decorrelates ranges/replicas)
+    const float* keep;    // [V] or nullptr (keep everything)
+    uint64_t key;         // subsampling stream key
+    uint32_t* tile_count; // [ntiles]
+    uint64_t* tile_off;   // [ntiles + 1]
+    int32_t* kept;        // [n] compacted kept ids
+    float* sent_alpha;    // [ceil(n / 1000) + 1]
+    // alpha schedule
+    uint64_t progress_base;
+    uint32_t progress_mult;
+    uint64_t total_words;
+    float alpha0;
+};
+int64_t sub_tiles(int64_t n);
+void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches);
+
+// ---------------- throughput mode: Hogwild training (K1) ----------------------
+struct HogArgs {
+    float* syn0;               // [V * Dp]
+    float* syn1;               // [(V-1) * Dp], rows in usage-rank order
+    int32_t d4;                // Dp / 4 (row stride in float4)
+    const int32_t* path_off;   // [V+1]
+    const int32_t* path_code;  // (row << 1) | turn
+    const int32_t* kept;
+    const uint64_t* n_kept_dev;  // device scalar written by the subsample kernels
+    const float* sent_alpha;
+    const float* sigmoid;      // [1000]
+    float sig_scale;
+    int32_t window;
+    uint64_t win_key;
+    int32_t cache_rows;        // K rows cached in shared memory (rows [0, K))
+    int32_t centers_per_warp;
+    unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
+};
+struct HogGeometry {
+    int warps;      // per block
+    int blocks;     // grid
+    int cpw;        // centers per warp per tile
+    int cache_rows;
+    int variant;    // DCH
+    size_t smem;
+};
+// Picks the kernel variant for d4 and the launch geometry for the device.
+HogGeometry hog_plan(int d4, int cache_rows_wanted, int warps_override, int cpw_override, int rows_override);
+void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
+
+}  // namespace cgk

@@ -1,0 +1,117 @@
+"""Throughput mode (K3 + K1) on the device: coverage, pair distribution and quality.
+
+Hogwild runs are not bit-reproducible (neither is the reference with workers > 1),
+so parity is checked through properties: every token counted, subsampling and the
+dynamic window produce the reference's pair distribution, and the north-star quality
+gates -- mean HS log-loss within 2% of the reference's, planted-cluster recall@10
+within 0.02 -- on seeded synthetic corpora."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_1606_07822_b200 import api
+from paper_1606_07822_b200.corpus_gen import CONFIGS, CorpusConfig, cluster_raw_ids, generate, vocab_from_raw
+
+pytestmark = pytest.mark.gpu
+
+
+def setup(vocab, k=31):
+    tree = api.build_huffman_tree(vocab)
+    return tree, api.select_cached_nodes(tree, k)
+
+
+def c1():
+    c = CONFIGS["c1"]
+    vocab, ids = vocab_from_raw(generate(c), c.min_count, c.vocab)
+    return c, vocab, ids
+
+
+def test_hogwild_covers_stream_and_matches_pair_distribution():
+    c, vocab, ids = c1()
+    tree, sel = setup(vocab)
+    cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1, seed=1)
+    s = api.Session(vocab, tree, sel, cfg)
+    s.upload_ids(ids)
+    e = s.train_range(0, 0, ids.size, 0, 1)
+    m = s.download()
+    s.close()
+    assert e.words == ids.size
+    assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
+    # expected kept tokens: sum of keep probabilities over the stream
+    kp = O.keep_table(vocab.counts, vocab.total_tokens(), c.sample)
+    expect_kept = float(kp[ids].astype(np.float64).sum())
+    assert abs(e.kept - expect_kept) / expect_kept < 0.005
+    # the reference's single-worker stream as the pair-count yardstick
+    _, _, ost = O.orc_train(ids, vocab.counts, vocab.total_tokens(),
+                            dict(dim=4, window=c.window, sample=c.sample, min_count=1, cache_nodes=0, seed=1))
+    assert abs(e.pairs - ost.pairs) / ost.pairs < 0.01
+    assert abs(e.steps - ost.steps) / ost.steps < 0.01
+
+
+def test_hogwild_multiple_ranges_cover_stream():
+    c, vocab, ids = c1()
+    tree, sel = setup(vocab, 0)
+    cfg = api.TrainConfig(dim=16, window=3, min_count=1, sample=0.0, iterations=1, seed=3)
+    s = api.Session(vocab, tree, sel, cfg)
+    s.upload_ids(ids)
+    cuts = [0, 12345, 500000, ids.size]
+    words = kept = 0
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        e = s.train_range(0, a, b, a, 1)
+        words += e.words
+        kept += e.kept
+    s.close()
+    assert words == ids.size and kept == ids.size  # sample 0 keeps everything
+
+
+def _loss(model, tree, vocab, ids, c, n=1 << 16, seed=12345):
+    cen, ctx = O.sample_pairs(ids, vocab.counts, vocab.total_tokens(), c.sample, c.window, seed, n)
+    t = O.Tree(tree.offsets, tree.nodes, tree.turns, tree.usage)
+    return O.hs_loss(cen, ctx, model.syn0, model.syn1, t)
+
+
+@pytest.mark.parametrize("k", [0, 31])
+def test_hogwild_loss_within_2pct_of_reference_c1(k):
+    c, vocab, ids = c1()
+    tree, sel = setup(vocab, k)
+    cfg = dict(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1, cache_nodes=k,
+               flush_interval=10, seed=1)
+    ref0, ref1, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
+    ref_loss = _loss(api.Model(vocab.size(), c.dim, ref0, ref1), tree, vocab, ids, c)
+    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg))
+    gpu_loss = _loss(m, tree, vocab, ids, c)
+    init = api.init_model(vocab.size(), c.dim, 1)
+    init_loss = _loss(init, tree, vocab, ids, c)
+    assert gpu_loss < init_loss * 0.9
+    assert abs(gpu_loss - ref_loss) / ref_loss < 0.02, (gpu_loss, ref_loss)
+
+
+def recall_at_10(syn0: np.ndarray, cluster: np.ndarray, sample: np.ndarray) -> float:
+    import torch
+    x = torch.tensor(syn0, device="cuda", dtype=torch.float32)
+    x = x / x.norm(dim=1, keepdim=True).clamp_min(1e-12)
+    q = x[torch.tensor(sample, device="cuda")]
+    sim = q @ x.T
+    sim[torch.arange(len(sample)), torch.tensor(sample, device="cuda")] = -2.0
+    top = sim.topk(10, dim=1).indices.cpu().numpy()
+    cl = cluster[sample][:, None]
+    return float((cluster[top] == cl).mean())
+
+
+def test_hogwild_planted_cluster_recall_matches_reference():
+    """A reduced C3 (1M tokens, 40 clusters x 50 words, D 64, 3 epochs)."""
+    cc = CorpusConfig("c3-mini", 1_000_000, 2000, 1.0, 64, 5, 1e-3, 3, 3, line_every=20, clusters=40,
+                      cluster_size=50, in_cluster=0.7)
+    raw, cluster_of = cluster_raw_ids(cc)
+    vocab, ids = vocab_from_raw(raw, 5, cc.clusters * cc.cluster_size)
+    tree, sel = setup(vocab)
+    cfg = dict(dim=cc.dim, window=cc.window, min_count=5, sample=cc.sample, iterations=3, cache_nodes=31,
+               flush_interval=10, seed=3)
+    r0, _, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
+    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg))
+    cluster = cluster_of[vocab.raw_of_id]
+    sample = np.arange(0, vocab.size(), 3)
+    r_ref = recall_at_10(r0, cluster, sample)
+    r_gpu = recall_at_10(m.syn0, cluster, sample)
+    assert r_ref > 0.3
+    assert abs(r_gpu - r_ref) <= 0.02, (r_gpu, r_ref)
