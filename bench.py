@@ -50,6 +50,9 @@ def parse():
     p.add_argument("--warps", type=int, default=0)
     p.add_argument("--cpw", type=int, default=0)
     p.add_argument("--rows", type=int, default=-1)
+    p.add_argument("--blocks", type=int, default=0)
+    p.add_argument("--cold-update", type=int, default=0)
+    p.add_argument("--hot-flush-scale", type=float, default=0.0)
     return p.parse_args()
 
 
@@ -234,7 +237,7 @@ def main():
                           cache_nodes=args.cache_nodes, seed=c.seed)
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
-    sess.tune(args.warps, args.cpw, args.rows)
+    sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale)
     sess.upload_ids(ids)
     model_t = sess.model_tensor() if world > 1 else None
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")

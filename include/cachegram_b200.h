@@ -186,8 +186,16 @@ CG_API int cg_session_train(cg_session* s, cg_train_stats* stats);
 CG_API int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out);
 /* The device model buffer (for an all-reduce between replicas) and its geometry. */
 CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int32_t* row_stride_floats);
-/* Overrides the hogwild kernel geometry (0 = auto). For tuning and tests. */
-CG_API int cg_session_tune(cg_session* s, int32_t warps_per_block, int32_t centers_per_warp, int32_t smem_cache_rows);
+/* Hogwild kernel knobs (zero-initialised = defaults). For tuning and experiments. */
+typedef struct cg_tuning {
+    int32_t blocks;           /* 0 = one persistent CTA per SM */
+    int32_t warps_per_block;  /* 0 = the variant's maximum */
+    int32_t centers_per_warp; /* 0 = 8: centers a warp trains between block-cache flushes */
+    int32_t smem_cache_rows;  /* < 0 = min(K, what fits); hot rows held in the block cache */
+    int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
+    float hot_flush_scale;    /* 0 = 1/blocks (model averaging of the per-CTA hot-row replicas) */
+} cg_tuning;
+CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 
 #ifdef __cplusplus
 }

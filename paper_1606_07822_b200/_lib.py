@@ -81,6 +81,11 @@ class CgEpochStats(C.Structure):
     ]
 
 
+class CgTuning(C.Structure):
+    _fields_ = [("blocks", C.c_int32), ("warps_per_block", C.c_int32), ("centers_per_warp", C.c_int32),
+                ("smem_cache_rows", C.c_int32), ("cold_update", C.c_int32), ("hot_flush_scale", C.c_float)]
+
+
 P = C.POINTER
 vp = C.c_void_p
 # name -> (restype, argtypes); mirrors include/cachegram_b200.h
@@ -120,7 +125,7 @@ SIGNATURES = {
     "cg_session_train": (C.c_int, [vp, P(CgTrainStats)]),
     "cg_session_download": (C.c_int, [vp, P(C.c_float), P(C.c_float)]),
     "cg_session_model_buffer": (C.c_int, [vp, P(vp), P(C.c_size_t), P(C.c_int32)]),
-    "cg_session_tune": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32]),
+    "cg_session_tune": (C.c_int, [vp, P(CgTuning)]),
 }
 
 _lib = None

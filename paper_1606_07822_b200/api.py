@@ -424,8 +424,10 @@ class Session:
         check(load().cg_session_set_model(self._h, ptr(np.ascontiguousarray(model.syn0), C.c_float),
                                           ptr(np.ascontiguousarray(model.syn1), C.c_float)))
 
-    def tune(self, warps: int = 0, centers_per_warp: int = 0, cache_rows: int = -1) -> None:
-        check(load().cg_session_tune(self._h, warps, centers_per_warp, cache_rows))
+    def tune(self, blocks: int = 0, warps: int = 0, centers_per_warp: int = 0, cache_rows: int = -1,
+             cold_update: int = 0, hot_flush_scale: float = 0.0) -> None:
+        t = _lib.CgTuning(blocks, warps, centers_per_warp, cache_rows, cold_update, hot_flush_scale)
+        check(load().cg_session_tune(self._h, C.byref(t)))
 
     def train_range(self, epoch: int, begin: int, end: int, progress_base: int = 0,
                     progress_mult: int = 1) -> CgEpochStats:

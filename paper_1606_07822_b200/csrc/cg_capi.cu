@@ -185,7 +185,7 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    int tune_warps = 0, tune_cpw = 0, tune_rows = -1;
+    cg_tuning tune{0, 0, 0, -1, 0, 0.0f};
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -539,11 +539,11 @@ int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int
     });
 }
 
-int cg_session_tune(cg_session* s, int32_t warps_per_block, int32_t centers_per_warp, int32_t smem_cache_rows) {
+int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
-        s->tune_warps = warps_per_block;
-        s->tune_cpw = centers_per_warp;
-        s->tune_rows = smem_cache_rows;
+        if (!t) invalid("null tuning");
+        if (t->cold_update < 0 || t->cold_update > 1) invalid("cold_update must be 0 or 1");
+        s->tune = *t;
     });
 }
 
@@ -617,7 +617,14 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.window = s->cfg.window;
             h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
             h.counters = s->counters.p;
-            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->K, s->tune_warps, s->tune_cpw, s->tune_rows);
+            h.cold_store = s->tune.cold_update;
+            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->K, s->tune.blocks, s->tune.warps_per_block,
+                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows);
+            // Each CTA trains its own replica of the hot rows between flushes; flushing
+            // delta / n_CTA averages the replicas (local SGD + model averaging, as across
+            // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every
+            // CTA pushes the same top-of-tree correction, overshooting by ~n_CTA.
+            h.hot_flush_scale = s->tune.hot_flush_scale > 0.0f ? s->tune.hot_flush_scale : 1.0f / static_cast<float>(g.blocks);
             CG_CUDA(cudaEventRecord(s->ev[2], s->stream));
             cgk::launch_hogwild(h, g, s->stream);
             CG_CUDA(cudaGetLastError());

@@ -63,6 +63,10 @@ __device__ __forceinline__ float4 ld_ca4(const float* p) {
                  : "l"(p));
     return r;
 }
+__device__ __forceinline__ void st_cg4(float* p, float4 v) {
+    asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 // Fire-and-forget vector atomic add at L2 (REDG.E.ADD.F32x4).
 __device__ __forceinline__ void red_add4(float* p, float4 v) {
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)

@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
                                     const size_t e = static_cast<size_t>(rows[g]) * d4 + q;
                                     if (rows[g] < K)
                                         dblk[e] = add4(dblk[e], gv);
+                                    else if (a.cold_store)
+                                        st_cg4(a.syn1 + 4 * e, add4(R[g][k], gv));
                                     else
                                         red_add4(a.syn1 + 4 * e, gv);
                                 }
@@ -293,7 +295,12 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
 #pragma unroll
                 for (int k = 0; k < DCH; ++k) {
                     const int q = lane + 32 * k;
-                    if (q < d4) red_add4(vrow + 4 * q, h[k]);
+                    if (q < d4) {
+                        if (a.cold_store)
+                            st_cg4(vrow + 4 * q, add4(v[k], h[k]));
+                        else
+                            red_add4(vrow + 4 * q, h[k]);
+                    }
                 }
                 ++n_pairs;
                 n_steps += static_cast<unsigned long long>(L);
@@ -327,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
             for (int i = tid; i < K * d4; i += blockDim.x) {
                 const float4 d = dblk[i];
                 if (nonzero4(d)) {
-                    red_add4(a.syn1 + 4 * static_cast<size_t>(i), d);
+                    red_add4(a.syn1 + 4 * static_cast<size_t>(i), scale4(a.hot_flush_scale, d));
                     dblk[i] = f4(0.f);
                 }
             }
@@ -378,7 +385,8 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
     if (launches) *launches = 3;
 }
 
-HogGeometry hog_plan(int d4, int cache_rows_wanted, int warps_override, int cpw_override, int rows_override) {
+HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
+                     int rows_override) {
     HogGeometry g{};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -386,7 +394,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int warps_override, int cpw_
     g.variant = (d4 + 31) / 32;
     const int threads = g.variant == 1 ? kThreadsD1 : (g.variant == 2 ? kThreadsD2 : kThreadsD3);
     g.warps = warps_override > 0 ? std::min(warps_override, threads / 32) : threads / 32;
-    g.blocks = sms;
+    g.blocks = blocks_override > 0 ? blocks_override : sms;
     g.cpw = cpw_override > 0 ? cpw_override : 8;
     // shared-memory cache budget ~110 KB so L1 keeps room for the hot-row bases
     const size_t budget = 110 * 1024;

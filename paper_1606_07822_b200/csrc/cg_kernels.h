@@ -104,6 +104,8 @@ struct HogArgs {
     uint64_t win_key;
     int32_t cache_rows;        // K rows cached in shared memory (rows [0, K))
     int32_t centers_per_warp;
+    int32_t cold_store;        // 1: plain stores for cold rows and syn0 (lossy Hogwild)
+    float hot_flush_scale;     // multiplier on block-cache deltas at flush
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
 struct HogGeometry {
@@ -115,7 +117,8 @@ struct HogGeometry {
     size_t smem;
 };
 // Picks the kernel variant for d4 and the launch geometry for the device.
-HogGeometry hog_plan(int d4, int cache_rows_wanted, int warps_override, int cpw_override, int rows_override);
+HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
+                     int rows_override);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 }  // namespace cgk
