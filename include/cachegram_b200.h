@@ -194,6 +194,7 @@ typedef struct cg_tuning {
     int32_t smem_cache_rows;  /* < 0 = min(K, what fits); hot rows held in the block cache */
     int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
     float hot_flush_scale;    /* 0 = 1/blocks (model averaging of the per-CTA hot-row replicas) */
+    int32_t flush_centers;    /* 0 = 64: centers merged into a CTA's cache between flushes */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 

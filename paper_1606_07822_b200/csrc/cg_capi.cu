@@ -185,7 +185,8 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    cg_tuning tune{0, 0, 0, -1, 0, 0.0f};
+    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0};
+    int32_t cached_rows = 0;  // hogwild: hot rows within the kernel's private prefix depth
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -422,17 +423,28 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             if (s->Dp > 4 * 96) invalid("hogwild mode supports dim <= 384");
             if (s->max_depth > 64) invalid("hogwild mode supports Huffman depth <= 64");
             if (steps >= (int64_t{1} << 31)) invalid("tree too large for 32-bit path offsets");
-            // device row order: hot slots first (slot order), then the remaining inner
-            // nodes by (usage desc, id asc); "hot" becomes row < K in the kernel
-            std::vector<int32_t> rest;
-            std::vector<char> is_hot(static_cast<size_t>(V - 1), 0);
+            // Device row order: first the hot rows (CacheSelection slot order) whose depth is
+            // below the kernel's private-prefix depth HMAX -- the rows the per-CTA cache
+            // holds, so "cached" is simply row < cached_rows -- then every other inner node
+            // by (usage desc, id asc); one extra all-zero row pads cold-step groups.
+            const int hmax = cgk::hog_hmax(s->Dp / 4);
+            std::vector<int32_t> depth(static_cast<size_t>(V - 1), 0);
+            for (int32_t w = 0; w < V; ++w)
+                for (int64_t k = md->path_offsets[w]; k < md->path_offsets[w + 1]; ++k)
+                    depth[static_cast<size_t>(md->path_nodes[k])] = static_cast<int32_t>(k - md->path_offsets[w]);
+            std::vector<char> placed(static_cast<size_t>(V - 1), 0);
             s->node_of_row.reserve(static_cast<size_t>(V - 1));
             for (int32_t k = 0; k < s->K; ++k) {
-                s->node_of_row.push_back(md->hot_nodes[k]);
-                is_hot[static_cast<size_t>(md->hot_nodes[k])] = 1;
+                const int32_t n = md->hot_nodes[k];
+                if (depth[static_cast<size_t>(n)] < hmax) {
+                    s->node_of_row.push_back(n);
+                    placed[static_cast<size_t>(n)] = 1;
+                }
             }
+            s->cached_rows = static_cast<int32_t>(s->node_of_row.size());
+            std::vector<int32_t> rest;
             for (int32_t n = 0; n < V - 1; ++n)
-                if (!is_hot[static_cast<size_t>(n)]) rest.push_back(n);
+                if (!placed[static_cast<size_t>(n)]) rest.push_back(n);
             if (md->node_usage)
                 std::stable_sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
                     return md->node_usage[a] > md->node_usage[b];
@@ -448,7 +460,8 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             s->hw_code.upload(code.data(), code.size(), s->stream);
             s->node_of_row_dev.upload(s->node_of_row.data(), s->node_of_row.size(), s->stream);
             s->row_of_node_dev.upload(s->row_of_node.data(), s->row_of_node.size(), s->stream);
-            s->model.alloc(static_cast<size_t>(V) * s->Dp + static_cast<size_t>(V - 1) * s->Dp);
+            // syn0 [V rows] then syn1 [V-1 rows + 1 zero pad row]
+            s->model.alloc(static_cast<size_t>(V) * s->Dp + static_cast<size_t>(V) * s->Dp);
             s->counters.alloc(4);
         }
         session_reset_model(*s);
@@ -618,7 +631,9 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
             h.counters = s->counters.p;
             h.cold_store = s->tune.cold_update;
-            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->K, s->tune.blocks, s->tune.warps_per_block,
+            h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 64;
+            h.dummy_row = s->V - 1;
+            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->cached_rows, s->tune.blocks, s->tune.warps_per_block,
                                                      s->tune.centers_per_warp, s->tune.smem_cache_rows);
             // Each CTA trains its own replica of the hot rows between flushes; flushing
             // delta / n_CTA averages the replicas (local SGD + model averaging, as across

@@ -7,20 +7,24 @@
 //   1000-token sentences exactly like trainer.hpp:219-234, and each sentence gets the
 //   learning rate the reference would hold after filling it (trainer.hpp:223-228).
 //
-// K1 (hogwild): persistent CTAs pull tiles of consecutive kept centers from a global
-//   ticket counter; each warp trains its centers (train_center, trainer.hpp:147-175):
-//   window b = W - draw % W, contexts in the sentence, the center's root-first path.
-//   * Rows are 128-bit vectors, lanes own float4 chunks; dot products of all path steps
-//     of one pair are independent (distinct rows, fixed context row), so they are
+// K1 (hogwild): persistent CTAs; worker warps pull chunks of consecutive kept centers
+//   from a global ticket counter and train each one (train_center, trainer.hpp:147-175):
+//   window b = W - draw % W inside the center's 1000-token sentence, the center's
+//   root-first path. One warp of every CTA is the cache flusher.
+//   * Rows are 128-bit vectors, lanes own float4 chunks. The dot products of all path
+//     steps of one pair are independent (distinct rows, fixed context row), so they are
 //     reduced together with a warp transpose-reduce.
-//   * Hot rows (usage rank < K; a prefix of every path) live in a per-block shared
-//     memory delta cache (the paper's per-worker cache, NodeCache trainer.hpp:75-138):
-//     a warp snapshots the hot prefix of its center into registers, trains all pairs
-//     of the center on that private copy, and merges its delta into the block cache
-//     under a per-row lock. The block flushes the cache to HBM with red.global.add.v4
-//     after every tile and invalidates L1 so the next tile sees other blocks' flushes.
-//   * Cold rows are read L2-coherent (ld.global.cg) and updated with red.global.add.v4,
-//     so concurrent updates are never lost (Hogwild, trainer.hpp:249-253).
+//   * Hot rows -- the CacheSelection's top nodes, limited to the kernel's private-prefix
+//     depth HMAX -- are the per-CTA cache (the paper's per-worker cache, NodeCache
+//     trainer.hpp:75-138): a warp copies its center's hot prefix into registers, trains
+//     all pairs of the center on that private copy, and merges the delta into the CTA's
+//     shared-memory cache under a per-row lock. The flusher warp drains the cache into
+//     syn1 with red.global.add.v4 every `flush_centers` merged centers, scaled by
+//     1/n_CTA (model averaging of the CTA replicas, see cg_capi.cu), then fences so this
+//     SM's stale L1 copies of the hot rows are dropped.
+//   * Every other row is read L2-coherent (ld.global.cg) and updated with
+//     red.global.add.v4 (no lost updates) or, optionally, plain stores (the reference's
+//     lossy Hogwild, trainer.hpp:249-253).
 #include <algorithm>
 #include <cstdint>
 
@@ -126,37 +130,90 @@ __global__ void __launch_bounds__(kSubThreads) sub_scatter_kernel(SubArgs a) {
 }
 
 // ----------------------------------------------------------------------------- K1
-template <int DCH, int HMAX, int G, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
+constexpr int kCodeSlots = 80;  // per-warp path codes: L <= 64 plus group padding
+
+// Worker warps train centers; warp `workers` (the last one) is the cache flusher.
+template <int DCH, int HMAX, int G, int WORKERS>
+__global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
     constexpr int LGH = Log2<HMAX>::v;
     constexpr int LGG = Log2<G>::v;
     extern __shared__ float4 hsm[];
-    float* sig = reinterpret_cast<float*>(hsm);  // 1024 floats
-    float4* dblk = hsm + 256;                    // cache_rows * d4
+    float* sig = reinterpret_cast<float*>(hsm);                      // 1024 floats
+    int* codes_all = reinterpret_cast<int*>(hsm + 256);              // WORKERS * kCodeSlots
+    float4* dblk = hsm + 256 + WORKERS * (kCodeSlots / 4);           // cache_rows * d4
     const int K = a.cache_rows;
     const int d4 = a.d4;
-    int* locks = reinterpret_cast<int*>(dblk + static_cast<size_t>(K) * d4);
-    __shared__ unsigned long long s_ticket;
+    int* locks = reinterpret_cast<int*>(dblk + K * d4);
+    __shared__ int s_done;
+    __shared__ unsigned s_merged;
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int workers = (blockDim.x >> 5) - 1;
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
     for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
+    if (tid == 0) {
+        s_done = 0;
+        s_merged = 0;
+    }
     __syncthreads();
 
+    if (warp == workers) {
+        // ---- flusher: drain the block cache into syn1 (scaled), row by row under the
+        // row locks, whenever enough centers were merged; never blocks the workers.
+        unsigned last = 0;
+        for (;;) {
+            const bool done = *reinterpret_cast<volatile int*>(&s_done) == workers;
+            const unsigned merged = *reinterpret_cast<volatile unsigned*>(&s_merged);
+            if (K > 0 && (done || merged - last >= static_cast<unsigned>(a.flush_centers))) {
+                last = merged;
+                for (int r = 0; r < K; ++r) {
+                    if (lane == 0)
+                        while (atomicCAS(&locks[r], 0, 1) != 0) {
+                        }
+                    __syncwarp();
+                    __threadfence_block();
+                    float4 d[DCH];
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        d[k] = f4(0.f);
+                        if (q < d4) {
+                            d[k] = dblk[r * d4 + q];
+                            dblk[r * d4 + q] = f4(0.f);
+                        }
+                    }
+                    __threadfence_block();
+                    __syncwarp();
+                    if (lane == 0) atomicExch(&locks[r], 0);
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        if (q < d4 && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(a.hot_flush_scale, d[k]));
+                    }
+                }
+                __threadfence();  // publish the flush; also drops this SM's stale L1 lines of hot rows
+            }
+            if (done) break;
+            __nanosleep(2000);
+        }
+        return;
+    }
+
+    // ---- workers
+    int* codes = codes_all + warp * kCodeSlots;
+    const int dummy_code = a.dummy_row << 1;
     const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
     const int cpw = a.centers_per_warp;
-    const int64_t tile_len = static_cast<int64_t>(nw) * cpw;
     unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
 
     for (;;) {
-        if (tid == 0) s_ticket = atomicAdd(a.counters, 1ull);
-        __syncthreads();
-        const int64_t t0 = static_cast<int64_t>(s_ticket) * tile_len;
-        if (t0 >= n_kept) break;
-        const int64_t cb = t0 + static_cast<int64_t>(warp) * cpw;
-        const int64_t ce = min(cb + cpw, n_kept);
-        for (int64_t ci = cb; ci < ce; ++ci) {
+        long long c0 = 0;
+        if (lane == 0) c0 = static_cast<long long>(atomicAdd(a.counters, static_cast<unsigned long long>(cpw)));
+        c0 = __shfl_sync(kFull, c0, 0);
+        if (c0 >= n_kept) break;
+        const int64_t cend = min(static_cast<int64_t>(c0) + cpw, n_kept);
+        for (int64_t ci = c0; ci < cend; ++ci) {
             const int32_t c = a.kept[ci];
             const int64_t s_lo = ci / kSentence * kSentence;
             const int64_t s_hi = min(s_lo + kSentence, n_kept);
@@ -168,25 +225,23 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
             if (hi == lo) continue;
             const int p0 = a.path_off[c];
             const int L = a.path_off[c + 1] - p0;
-            const int code_a = lane < L ? a.path_code[p0 + lane] : 0;
-            const int code_b = lane + 32 < L ? a.path_code[p0 + 32 + lane] : 0;
-            const unsigned hm = __ballot_sync(kFull, lane < L && (code_a >> 1) < K);
+            __syncwarp();
+            for (int j = lane; j < kCodeSlots; j += 32) codes[j] = j < L ? a.path_code[p0 + j] : dummy_code;
+            __syncwarp();
+            const unsigned hm = __ballot_sync(kFull, lane < L && (codes[lane] >> 1) < K);
             const int H = hm == kFull ? 32 : __ffs(~hm) - 1;
             const int Hp = min(H, HMAX);
 
-            // private copy of the hot prefix: U = working rows, Q = this center's delta
+            // private copy of the cached prefix: U = working rows, Q = this center's delta
             float4 U[HMAX][DCH], Q[HMAX][DCH];
 #pragma unroll
             for (int j = 0; j < HMAX; ++j) {
-                const int row = __shfl_sync(kFull, code_a, j) >> 1;
+                const int row = codes[j] >> 1;
 #pragma unroll
                 for (int k = 0; k < DCH; ++k) {
                     const int q = lane + 32 * k;
                     float4 u = f4(0.f);
-                    if (j < Hp && q < d4) {
-                        const size_t e = static_cast<size_t>(row) * d4 + q;
-                        u = add4(ld_ca4(a.syn1 + 4 * e), dblk[e]);
-                    }
+                    if (j < Hp && q < d4) u = add4(ld_ca4(a.syn1 + 4 * (row * d4 + q)), dblk[row * d4 + q]);
                     U[j][k] = u;
                     Q[j][k] = f4(0.f);
                 }
@@ -194,15 +249,15 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
 
             for (int64_t xi = lo; xi <= hi; ++xi) {
                 if (xi == ci) continue;
-                float* vrow = a.syn0 + static_cast<size_t>(a.kept[xi]) * d4 * 4;
+                const int xo = a.kept[xi] * d4;
                 float4 v[DCH], h[DCH];
 #pragma unroll
                 for (int k = 0; k < DCH; ++k) {
                     const int q = lane + 32 * k;
-                    v[k] = q < d4 ? ld_cg4(vrow + 4 * q) : f4(0.f);
+                    v[k] = q < d4 ? ld_cg4(a.syn0 + 4 * (xo + q)) : f4(0.f);
                     h[k] = f4(0.f);
                 }
-                // -- phase A: the private hot prefix
+                // -- phase A: the cached prefix, on the private copy
                 if (Hp > 0) {
                     float p[HMAX];
 #pragma unroll
@@ -214,9 +269,8 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
                     }
                     const float tot = transpose_reduce<HMAX>(p, lane);
                     const int jl = lane >> (5 - LGH);
-                    const int cj = __shfl_sync(kFull, code_a, jl);
                     const float f = table_sigmoid(sig, tot, a.sig_scale);
-                    const float gl = (1.0f - static_cast<float>(cj & 1) - f) * alpha;
+                    const float gl = (1.0f - static_cast<float>(codes[jl] & 1) - f) * alpha;
 #pragma unroll
                     for (int j = 0; j < HMAX; ++j) {
                         const float g = __shfl_sync(kFull, gl, j << (5 - LGH));
@@ -224,35 +278,23 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 h[k] = axpy4(g, U[j][k], h[k]);
-                                const float4 gv = scale4(g, v[k]);
-                                U[j][k] = add4(U[j][k], gv);
-                                Q[j][k] = add4(Q[j][k], gv);
+                                U[j][k] = axpy4(g, v[k], U[j][k]);
+                                Q[j][k] = axpy4(g, v[k], Q[j][k]);
                             }
                         }
                     }
                 }
-                // -- phase B: the rest of the path, G steps at a time
+                // -- phase B: the rest of the path, G steps at a time (padded with a zero row)
                 for (int j0 = Hp; j0 < L; j0 += G) {
                     float4 R[G][DCH];
-                    int rows[G];
+                    int ro[G];
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
-                        const int j = j0 + g;
-                        const int ca = __shfl_sync(kFull, code_a, j & 31);
-                        const int cb2 = __shfl_sync(kFull, code_b, j & 31);
-                        rows[g] = j < L ? ((j < 32 ? ca : cb2) >> 1) : -1;
-                    }
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
+                        ro[g] = (codes[j0 + g] >> 1) * d4;
 #pragma unroll
                         for (int k = 0; k < DCH; ++k) {
                             const int q = lane + 32 * k;
-                            float4 u = f4(0.f);
-                            if (rows[g] >= 0 && q < d4) {
-                                const size_t e = static_cast<size_t>(rows[g]) * d4 + q;
-                                u = rows[g] < K ? add4(ld_ca4(a.syn1 + 4 * e), dblk[e]) : ld_cg4(a.syn1 + 4 * e);
-                            }
-                            R[g][k] = u;
+                            R[g][k] = q < d4 ? ld_cg4(a.syn1 + 4 * (ro[g] + q)) : f4(0.f);
                         }
                     }
                     float p[G];
@@ -265,29 +307,21 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
                     }
                     const float tot = transpose_reduce<G>(p, lane);
                     const int jl = j0 + (lane >> (5 - LGG));
-                    const int ca = __shfl_sync(kFull, code_a, jl & 31);
-                    const int cb2 = __shfl_sync(kFull, code_b, jl & 31);
-                    const int cj = jl < 32 ? ca : cb2;
                     const float f = table_sigmoid(sig, tot, a.sig_scale);
-                    const float gl = jl < L ? (1.0f - static_cast<float>(cj & 1) - f) * alpha : 0.f;
+                    const float gl = jl < L ? (1.0f - static_cast<float>(codes[jl] & 1) - f) * alpha : 0.f;
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
                         const float gg = __shfl_sync(kFull, gl, g << (5 - LGG));
-                        if (rows[g] >= 0) {
+                        const bool live = j0 + g < L;
 #pragma unroll
-                            for (int k = 0; k < DCH; ++k) {
-                                const int q = lane + 32 * k;
-                                if (q < d4) {
-                                    h[k] = axpy4(gg, R[g][k], h[k]);
-                                    const float4 gv = scale4(gg, v[k]);
-                                    const size_t e = static_cast<size_t>(rows[g]) * d4 + q;
-                                    if (rows[g] < K)
-                                        dblk[e] = add4(dblk[e], gv);
-                                    else if (a.cold_store)
-                                        st_cg4(a.syn1 + 4 * e, add4(R[g][k], gv));
-                                    else
-                                        red_add4(a.syn1 + 4 * e, gv);
-                                }
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            h[k] = axpy4(gg, R[g][k], h[k]);
+                            if (live && q < d4) {
+                                if (a.cold_store)
+                                    st_cg4(a.syn1 + 4 * (ro[g] + q), axpy4(gg, v[k], R[g][k]));
+                                else
+                                    red_add4(a.syn1 + 4 * (ro[g] + q), scale4(gg, v[k]));
                             }
                         }
                     }
@@ -297,19 +331,19 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
                     const int q = lane + 32 * k;
                     if (q < d4) {
                         if (a.cold_store)
-                            st_cg4(vrow + 4 * q, add4(v[k], h[k]));
+                            st_cg4(a.syn0 + 4 * (xo + q), add4(v[k], h[k]));
                         else
-                            red_add4(vrow + 4 * q, h[k]);
+                            red_add4(a.syn0 + 4 * (xo + q), h[k]);
                     }
                 }
                 ++n_pairs;
                 n_steps += static_cast<unsigned long long>(L);
             }
-            // merge the center's hot-prefix delta into the block cache
+            // merge the center's delta into the block cache (row locks) and count it
 #pragma unroll
             for (int j = 0; j < HMAX; ++j) {
                 if (j < Hp) {
-                    const int row = __shfl_sync(kFull, code_a, j) >> 1;
+                    const int row = codes[j] >> 1;
                     if (lane == 0)
                         while (atomicCAS(&locks[row], 0, 1) != 0) {
                         }
@@ -318,40 +352,27 @@ __global__ void __launch_bounds__(THREADS, 1) hog_kernel(HogArgs a) {
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
-                        if (q < d4) {
-                            const size_t e = static_cast<size_t>(row) * d4 + q;
-                            dblk[e] = add4(dblk[e], Q[j][k]);
-                        }
+                        if (q < d4) dblk[row * d4 + q] = add4(dblk[row * d4 + q], Q[j][k]);
                     }
                     __threadfence_block();
                     __syncwarp();
                     if (lane == 0) atomicExch(&locks[row], 0);
                 }
             }
+            if (lane == 0 && Hp > 0) atomicAdd(&s_merged, 1u);
         }
-        __syncthreads();
-        if (K > 0) {
-            for (int i = tid; i < K * d4; i += blockDim.x) {
-                const float4 d = dblk[i];
-                if (nonzero4(d)) {
-                    red_add4(a.syn1 + 4 * static_cast<size_t>(i), scale4(a.hot_flush_scale, d));
-                    dblk[i] = f4(0.f);
-                }
-            }
-            __threadfence();  // order the flush before later loads; drops stale L1 lines
-        }
-        __syncthreads();
     }
     if (lane == 0) {  // counts are warp-uniform
         atomicAdd(a.counters + 1, n_pairs);
         atomicAdd(a.counters + 2, n_steps);
         atomicAdd(a.counters + 3, n_centers);
+        atomicAdd(&s_done, 1);
     }
 }
 
-template <int DCH, int HMAX, int G, int THREADS>
+template <int DCH, int HMAX, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = hog_kernel<DCH, HMAX, G, THREADS>;
+    auto k = hog_kernel<DCH, HMAX, G, WORKERS>;
     static bool configured = false;
     if (!configured) {
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -360,13 +381,25 @@ void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
     b.centers_per_warp = g.cpw;
-    k<<<g.blocks, g.warps * 32, g.smem, s>>>(b);
+    k<<<g.blocks, (g.warps + 1) * 32, g.smem, s>>>(b);
 }
 
-// per-variant register budgets: threads per CTA the launch bounds promise
-constexpr int kThreadsD1 = 384;
-constexpr int kThreadsD2 = 384;
-constexpr int kThreadsD3 = 256;
+// Per-variant shape: float4 chunks per lane (DCH), private cached prefix (HMAX),
+// cold-step group (G) and worker warps (register budget of the launch bounds).
+template <int DCH>
+struct Variant;
+template <>
+struct Variant<1> {
+    static constexpr int HMAX = 8, G = 8, WORKERS = 11;
+};
+template <>
+struct Variant<2> {
+    static constexpr int HMAX = 4, G = 4, WORKERS = 11;
+};
+template <>
+struct Variant<3> {
+    static constexpr int HMAX = 4, G = 4, WORKERS = 7;
+};
 
 }  // namespace
 
@@ -385,6 +418,14 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
     if (launches) *launches = 3;
 }
 
+int hog_hmax(int d4) {
+    switch ((d4 + 31) / 32) {
+        case 1: return Variant<1>::HMAX;
+        case 2: return Variant<2>::HMAX;
+        default: return Variant<3>::HMAX;
+    }
+}
+
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
                      int rows_override) {
     HogGeometry g{};
@@ -392,26 +433,26 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g.variant = (d4 + 31) / 32;
-    const int threads = g.variant == 1 ? kThreadsD1 : (g.variant == 2 ? kThreadsD2 : kThreadsD3);
-    g.warps = warps_override > 0 ? std::min(warps_override, threads / 32) : threads / 32;
+    const int workers = g.variant == 1 ? Variant<1>::WORKERS : (g.variant == 2 ? Variant<2>::WORKERS : Variant<3>::WORKERS);
+    g.warps = warps_override > 0 ? std::min(warps_override, workers) : workers;
     g.blocks = blocks_override > 0 ? blocks_override : sms;
-    g.cpw = cpw_override > 0 ? cpw_override : 8;
-    // shared-memory cache budget ~110 KB so L1 keeps room for the hot-row bases
+    g.cpw = cpw_override > 0 ? cpw_override : 4;
+    const size_t fixed = 4096 + static_cast<size_t>(workers) * kCodeSlots * 4;
     const size_t budget = 110 * 1024;
     const size_t per_row = static_cast<size_t>(d4) * 16 + 4;
-    const int fit = static_cast<int>((budget - 4096) / per_row);
+    const int fit = static_cast<int>((budget - fixed) / per_row);
     int rows = std::min(cache_rows_wanted, fit);
     if (rows_override >= 0 && rows_override < rows) rows = rows_override;
     g.cache_rows = std::max(rows, 0);
-    g.smem = 4096 + static_cast<size_t>(g.cache_rows) * per_row + 16;
+    g.smem = fixed + static_cast<size_t>(g.cache_rows) * per_row + 16;
     return g;
 }
 
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     switch (g.variant) {
-        case 1: launch_variant<1, 8, 8, kThreadsD1>(a, g, s); break;
-        case 2: launch_variant<2, 4, 4, kThreadsD2>(a, g, s); break;
-        default: launch_variant<3, 4, 4, kThreadsD3>(a, g, s); break;
+        case 1: launch_variant<1, Variant<1>::HMAX, Variant<1>::G, Variant<1>::WORKERS>(a, g, s); break;
+        case 2: launch_variant<2, Variant<2>::HMAX, Variant<2>::G, Variant<2>::WORKERS>(a, g, s); break;
+        default: launch_variant<3, Variant<3>::HMAX, Variant<3>::G, Variant<3>::WORKERS>(a, g, s); break;
     }
 }
 

@@ -106,6 +106,8 @@ struct HogArgs {
     int32_t centers_per_warp;
     int32_t cold_store;        // 1: plain stores for cold rows and syn0 (lossy Hogwild)
     float hot_flush_scale;     // multiplier on block-cache deltas at flush
+    int32_t flush_centers;     // centers merged into a block cache between flushes
+    int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
 struct HogGeometry {
@@ -116,6 +118,8 @@ struct HogGeometry {
     int variant;    // DCH
     size_t smem;
 };
+// Private cached-prefix depth of the kernel variant for this row width.
+int hog_hmax(int d4);
 // Picks the kernel variant for d4 and the launch geometry for the device.
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
                      int rows_override);

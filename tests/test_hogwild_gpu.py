@@ -82,7 +82,9 @@ def test_hogwild_loss_within_2pct_of_reference_c1(k):
     gpu_loss = _loss(m, tree, vocab, ids, c)
     init = api.init_model(vocab.size(), c.dim, 1)
     init_loss = _loss(init, tree, vocab, ids, c)
-    assert gpu_loss < init_loss * 0.9
+    # at least 90% of the reference's improvement over the initial model ...
+    assert init_loss - gpu_loss > 0.9 * (init_loss - ref_loss), (gpu_loss, ref_loss, init_loss)
+    # ... and the north-star gate
     assert abs(gpu_loss - ref_loss) / ref_loss < 0.02, (gpu_loss, ref_loss)
 
 
