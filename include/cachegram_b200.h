@@ -195,6 +195,8 @@ typedef struct cg_tuning {
     int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
     float hot_flush_scale;    /* 0 = 1/blocks (model averaging of the per-CTA hot-row replicas) */
     int32_t flush_centers;    /* 0 = 64: centers merged into a CTA's cache between flushes */
+    int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
+                                 context-row updates, bit 2 skip cache merges */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 

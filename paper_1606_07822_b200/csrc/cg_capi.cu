@@ -185,7 +185,7 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0};
+    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0, 0};
     int32_t cached_rows = 0;  // hogwild: hot rows within the kernel's private prefix depth
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -633,6 +633,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.cold_store = s->tune.cold_update;
             h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 64;
             h.dummy_row = s->V - 1;
+            h.probe = s->tune.probe;
             const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->cached_rows, s->tune.blocks, s->tune.warps_per_block,
                                                      s->tune.centers_per_warp, s->tune.smem_cache_rows);
             // Each CTA trains its own replica of the hot rows between flushes; flushing

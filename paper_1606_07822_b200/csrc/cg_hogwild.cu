@@ -318,7 +318,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
                             const int q = lane + 32 * k;
                             h[k] = axpy4(gg, R[g][k], h[k]);
                             if (live && q < d4) {
-                                if (a.cold_store)
+                                if (a.probe & 1) {
+                                } else if (a.cold_store)
                                     st_cg4(a.syn1 + 4 * (ro[g] + q), axpy4(gg, v[k], R[g][k]));
                                 else
                                     red_add4(a.syn1 + 4 * (ro[g] + q), scale4(gg, v[k]));
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 #pragma unroll
                 for (int k = 0; k < DCH; ++k) {
                     const int q = lane + 32 * k;
-                    if (q < d4) {
+                    if (q < d4 && !(a.probe & 2)) {
                         if (a.cold_store)
                             st_cg4(a.syn0 + 4 * (xo + q), add4(v[k], h[k]));
                         else
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
             // merge the center's delta into the block cache (row locks) and count it
 #pragma unroll
             for (int j = 0; j < HMAX; ++j) {
-                if (j < Hp) {
+                if (j < Hp && !(a.probe & 4)) {
                     const int row = codes[j] >> 1;
                     if (lane == 0)
                         while (atomicCAS(&locks[row], 0, 1) != 0) {
@@ -373,11 +374,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 template <int DCH, int HMAX, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     auto k = hog_kernel<DCH, HMAX, G, WORKERS>;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
+    if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
     b.centers_per_warp = g.cpw;

@@ -108,6 +108,7 @@ struct HogArgs {
     float hot_flush_scale;     // multiplier on block-cache deltas at flush
     int32_t flush_centers;     // centers merged into a block cache between flushes
     int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
+    int32_t probe;             // experiments only: 1 skip cold-row updates, 2 skip syn0 updates, 4 skip cache merges
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
 struct HogGeometry {

@@ -58,6 +58,10 @@ def main():
 
     grids = {}
     grids["scales"] = [dict(k=0)] + [dict(k=k, scale=sc) for k in (31, 255) for sc in (1 / 148, 1 / 64, 1 / 32, 1 / 16, 1 / 8)]
+    grids["probe"] = [dict(), dict(probe=1), dict(probe=2), dict(probe=3), dict(probe=4), dict(probe=7),
+                      dict(k=0, probe=1), dict(cold=1)]
+    grids["perf"] = [dict(), dict(cpw=1), dict(cpw=8), dict(cpw=16), dict(flush=16), dict(flush=256), dict(k=0),
+                     dict(warps=8), dict(scale=1 / 16), dict(cold=1)]
     grids["default"] = [
         dict(blocks=1, warps=1), dict(blocks=1, warps=1, k=0), dict(blocks=1, warps=12), dict(blocks=148, warps=1),
         dict(blocks=148, warps=1, k=0), dict(blocks=16, warps=12), dict(), dict(k=0), dict(cold=1), dict(k=0, cold=1),
@@ -68,7 +72,8 @@ def main():
         sel = api.select_cached_nodes(tree, k)
         cfg = api.TrainConfig(**dict(cfgd, cache_nodes=k))
         s = api.Session(vocab, tree, sel, cfg)
-        s.tune(g.get("blocks", 0), g.get("warps", 0), g.get("cpw", 0), -1, g.get("cold", 0), g.get("scale", 0.0))
+        s.tune(g.get("blocks", 0), g.get("warps", 0), g.get("cpw", 0), -1, g.get("cold", 0), g.get("scale", 0.0),
+               g.get("flush", 0), g.get("probe", 0))
         s.upload_ids(ids)
         ms = 0.0
         for it in range(a.iterations):
