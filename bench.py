@@ -64,30 +64,51 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ workload
-def workload(cfg_name: str, rank: int, world: int):
+def workload(cfg_name: str, rank: int, world: int, device: bool = False):
     """Per-rank shard of the configured corpus plus the shared vocabulary/tree.
     Each rank's shard has the configuration's full token count (weak scaling) and is
     drawn with its own seed; the vocabulary comes from shard 0 with ties broken by
-    raw rank, so every rank builds the identical tree without communication."""
-    from paper_1606_07822_b200.corpus_gen import CONFIGS, cluster_raw_ids, vocab_from_raw, zipf_raw_ids
+    first occurrence in shard 0, so every rank builds the identical tree without
+    communication. C4/C5 are generated on the GPU (`device=True`): ids come back as a
+    CUDA int32 tensor, otherwise as a numpy array."""
+    from paper_1606_07822_b200 import corpus_gen as G
 
-    c = CONFIGS[cfg_name]
+    c = G.CONFIGS[cfg_name]
+    if device and not c.clusters:
+        import torch
+
+        raw0 = G.zipf_raw_ids_device(c.tokens, c.vocab, c.zipf_s, c.seed)
+        vocab, ids0 = G.vocab_from_raw_device(raw0, c.min_count, c.vocab)
+        del raw0
+        if rank == 0:
+            return c, vocab, ids0
+        raw = G.zipf_raw_ids_device(c.tokens, c.vocab, c.zipf_s, c.seed * 1000 + rank)
+        rank_of = torch.full((c.vocab,), -1, dtype=torch.int32, device=raw.device)
+        rank_of[torch.from_numpy(vocab.raw_of_id).to(raw.device).long()] = torch.arange(
+            vocab.size(), dtype=torch.int32, device=raw.device)
+        ids = rank_of[raw.long()]
+        return c, vocab, ids[ids >= 0].contiguous()
     if c.clusters:
-        raw0, _ = cluster_raw_ids(c)
+        raw0, _ = G.cluster_raw_ids(c)
         space = c.clusters * c.cluster_size
     else:
-        raw0 = zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed)
+        raw0 = G.zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed)
         space = c.vocab
-    vocab, ids0 = vocab_from_raw(raw0, c.min_count, space)
+    vocab, ids0 = G.vocab_from_raw(raw0, c.min_count, space)
     if rank == 0:
-        ids = ids0
-    else:
-        raw = zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed * 1000 + rank) if not c.clusters else raw0
-        rank_of = np.full(space, -1, np.int32)
-        rank_of[vocab.raw_of_id] = np.arange(vocab.size(), dtype=np.int32)
-        ids = rank_of[raw]
-        ids = np.ascontiguousarray(ids[ids >= 0])
-    return c, vocab, ids
+        return c, vocab, ids0
+    raw = G.zipf_raw_ids(c.tokens, c.vocab, c.zipf_s, c.seed * 1000 + rank) if not c.clusters else raw0
+    rank_of = np.full(space, -1, np.int32)
+    rank_of[vocab.raw_of_id] = np.arange(vocab.size(), dtype=np.int32)
+    ids = rank_of[raw]
+    return c, vocab, np.ascontiguousarray(ids[ids >= 0])
+
+
+def host_ids(ids, n: int | None = None) -> np.ndarray:
+    if isinstance(ids, np.ndarray):
+        return ids if n is None else ids[:n]
+    t = ids if n is None else ids[:n]
+    return t.cpu().numpy()
 
 
 # ------------------------------------------------------------------ clocks
@@ -152,7 +173,8 @@ def reference_sample(c, vocab, ids, sample_tokens: int, workdir: str):
 
     import oracle_lib as O
 
-    n = min(sample_tokens, ids.size)
+    n = min(sample_tokens, len(ids))
+    ids = host_ids(ids, n)
     path = os.path.join(workdir, f"ref_sample_{c.name}.txt")
     words = np.array([b"w%d" % i for i in range(vocab.size())], dtype=object)
     with open(path, "wb") as f:
@@ -178,6 +200,14 @@ def run_reference(c, vocab, ids, threads: int, sample_tokens: int, reps: int, ca
     return rates, walls, n
 
 
+def _has_cuda() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -186,9 +216,8 @@ def cpu_threads() -> int:
 
 
 def auto_sample(c) -> int:
-    # ~10-30 s of reference CPU work on a many-core host; scaled by D*L per word
-    per_word = {"c1": 1.0, "c2": 2.0, "c3": 3.0, "c4": 6.0, "c5": 1.0}[c.name]
-    return int(min(c.tokens, 4_000_000 / per_word))
+    """Tokens per reference pass: about 10-30 s of CPU work on a 16-32 core host."""
+    return {"c1": 1_000_000, "c2": 17_000_000, "c3": 20_000_000, "c4": 6_000_000, "c5": 20_000_000}[c.name]
 
 
 # ------------------------------------------------------------------ main
@@ -199,7 +228,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        c, vocab, ids = workload(args.config, 0, 1)
+        c, vocab, ids = workload(args.config, 0, 1, device=args.config in ("c4", "c5") and _has_cuda())
         threads = cpu_threads()
         sample = args.cpu_sample_tokens or auto_sample(c)
         for _ in range(max(args.warmup, 0) and 1):
@@ -230,7 +259,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1606_07822_b200 import api
 
-    c, vocab, ids = workload(args.config, rank, world)
+    c, vocab, ids = workload(args.config, rank, world, device=args.config in ("c4", "c5"))
     tree = api.build_huffman_tree(vocab)
     sel = api.select_cached_nodes(tree, args.cache_nodes)
     cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
@@ -238,11 +267,14 @@ def main():
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
     sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale)
-    sess.upload_ids(ids)
+    if isinstance(ids, np.ndarray):
+        sess.upload_ids(ids)
+    else:
+        sess.upload_ids_device(ids)
     model_t = sess.model_tensor() if world > 1 else None
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
-    T = ids.size
+    T = int(len(ids))
     chunks = [(a, min(T, a + args.sync_words)) for a in range(0, T, args.sync_words)] if world > 1 else [(0, T)]
     launches = {"n": 0}
     agg = {"train_ms": 0.0, "bytes": 0.0, "pairs": 0, "steps": 0, "kept": 0, "launch_count": 0}
@@ -309,7 +341,7 @@ def main():
     # end to end through the public API: host ids in (pinned), host model out (pinned)
     e2e = None
     if args.e2e_steps > 0:
-        ids_pin = torch.from_numpy(ids).pin_memory()
+        ids_pin = torch.from_numpy(host_ids(ids)).pin_memory()
         out0 = torch.empty((vocab.size(), c.dim), dtype=torch.float32).pin_memory()
         out1 = torch.empty((vocab.size() - 1, c.dim), dtype=torch.float32).pin_memory()
         from paper_1606_07822_b200._lib import CgTrainStats, check, load, ptr
@@ -330,7 +362,7 @@ def main():
             t = torch.tensor([e2e_wall], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_wall = float(t.item())
-        e2e = {"value": float(T) * world / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": int(ids.nbytes),
+        e2e = {"value": float(T) * world / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": int(T * 4),
                "d2h_bytes_per_step": int(out0.numel() * 4 + out1.numel() * 4),
                "note": "cg_train(): host ids -> device, model init, subsample + train, device -> host model"}
 

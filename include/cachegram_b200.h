@@ -170,6 +170,8 @@ CG_API int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_
 CG_API void cg_session_destroy(cg_session* s);
 /* Copies the host id stream into device memory owned by the session. */
 CG_API int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids);
+/* Same from a device buffer (device-to-device copy; ids must already be valid). */
+CG_API int cg_session_upload_ids_device(cg_session* s, const int32_t* device_ids, int64_t n_ids);
 /* (Re)initialises the model on the device side from init_model(V, dim, seed). */
 CG_API int cg_session_reset_model(cg_session* s);
 /* Uploads a model given in reference layout (host). */

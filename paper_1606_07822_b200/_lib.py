@@ -119,6 +119,7 @@ SIGNATURES = {
     "cg_session_create": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), C.c_int32, vp, P(vp)]),
     "cg_session_destroy": (None, [vp]),
     "cg_session_upload_ids": (C.c_int, [vp, P(C.c_int32), C.c_int64]),
+    "cg_session_upload_ids_device": (C.c_int, [vp, vp, C.c_int64]),
     "cg_session_reset_model": (C.c_int, [vp]),
     "cg_session_set_model": (C.c_int, [vp, P(C.c_float), P(C.c_float)]),
     "cg_session_train_range": (C.c_int, [vp, C.c_int32, C.c_int64, C.c_int64, C.c_uint64, C.c_uint32,

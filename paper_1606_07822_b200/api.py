@@ -417,6 +417,12 @@ class Session:
         check(load().cg_session_upload_ids(self._h, ptr(ids, C.c_int32), ids.size))
         self.n_ids = int(ids.size)
 
+    def upload_ids_device(self, ids_tensor) -> None:
+        """Device-to-device copy of a CUDA int32 tensor of vocabulary ids."""
+        assert ids_tensor.is_cuda and ids_tensor.dtype.itemsize == 4 and ids_tensor.is_contiguous()
+        check(load().cg_session_upload_ids_device(self._h, C.c_void_p(ids_tensor.data_ptr()), ids_tensor.numel()))
+        self.n_ids = int(ids_tensor.numel())
+
     def reset_model(self) -> None:
         check(load().cg_session_reset_model(self._h))
 

@@ -478,6 +478,19 @@ void cg_session_destroy(cg_session* s) {
     delete s;
 }
 
+namespace {
+void session_alloc_stream(cg_session* s, int64_t n_ids) {
+    s->n_ids = n_ids;
+    if (s->mode == CG_MODE_HOGWILD) {
+        s->kept.alloc(static_cast<size_t>(std::max<int64_t>(n_ids, 1)));
+        s->sent_alpha.alloc(static_cast<size_t>(n_ids / cgdev::kSentence + 2));
+        const int64_t nt = cgk::sub_tiles(n_ids);
+        s->tile_count.alloc(static_cast<size_t>(std::max<int64_t>(nt, 1)));
+        s->tile_off.alloc(static_cast<size_t>(nt + 1));
+    }
+}
+}  // namespace
+
 int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids) {
     return guarded([&] {
         if (n_ids < 0) invalid("negative id count");
@@ -485,14 +498,20 @@ int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids) {
         for (int64_t i = 0; i < n_ids; ++i)
             if (ids[i] < 0 || ids[i] >= s->V) invalid("id out of vocabulary range");
         s->ids.upload(ids, static_cast<size_t>(n_ids), s->stream);
-        s->n_ids = n_ids;
-        if (s->mode == CG_MODE_HOGWILD) {
-            s->kept.alloc(static_cast<size_t>(std::max<int64_t>(n_ids, 1)));
-            s->sent_alpha.alloc(static_cast<size_t>(n_ids / cgdev::kSentence + 2));
-            const int64_t nt = cgk::sub_tiles(n_ids);
-            s->tile_count.alloc(static_cast<size_t>(std::max<int64_t>(nt, 1)));
-            s->tile_off.alloc(static_cast<size_t>(nt + 1));
-        }
+        session_alloc_stream(s, n_ids);
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_upload_ids_device(cg_session* s, const int32_t* device_ids, int64_t n_ids) {
+    return guarded([&] {
+        if (n_ids < 0) invalid("negative id count");
+        CG_CUDA(cudaSetDevice(s->device));
+        s->ids.alloc(static_cast<size_t>(n_ids));
+        if (n_ids)
+            CG_CUDA(cudaMemcpyAsync(s->ids.p, device_ids, static_cast<size_t>(n_ids) * 4, cudaMemcpyDeviceToDevice,
+                                    s->stream));
+        session_alloc_stream(s, n_ids);
         CG_CUDA(cudaStreamSynchronize(s->stream));
     });
 }
