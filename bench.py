@@ -275,23 +275,29 @@ def main():
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     T = int(len(ids))
-    chunks = [(a, min(T, a + args.sync_words)) for a in range(0, T, args.sync_words)] if world > 1 else [(0, T)]
     launches = {"n": 0}
     agg = {"train_ms": 0.0, "bytes": 0.0, "pairs": 0, "steps": 0, "kept": 0, "launch_count": 0}
+    record = {"on": False}
 
-    def one_step(epoch: int, record: bool):
-        for a, b in chunks:
-            e = sess.train_range(epoch, a, b, progress_base=a * world, progress_mult=world)
-            if record:
-                launches["n"] += e.train_launches + e.other_launches
-                agg["train_ms"] += e.train_ms
-                agg["bytes"] += 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs)
-                agg["pairs"] += e.pairs
-                agg["steps"] += e.steps
-                agg["kept"] += e.kept
-                agg["launch_count"] += e.train_launches
-            if world > 1:
-                dist.all_reduce(model_t, op=dist.ReduceOp.AVG)
+    def local_step(epoch, a, b, base, mult):
+        e = sess.train_range(epoch, a, b, base, mult)
+        if record["on"]:
+            launches["n"] += e.train_launches + e.other_launches
+            agg["train_ms"] += e.train_ms
+            agg["bytes"] += 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs)
+            agg["pairs"] += e.pairs
+            agg["steps"] += e.steps
+            agg["kept"] += e.kept
+            agg["launch_count"] += e.train_launches
+        return e
+
+    from paper_1606_07822_b200.replicas import ReplicaTrainer
+
+    trainer = ReplicaTrainer(local_step, model_t, world, rank, args.sync_words)
+
+    def one_step(epoch: int, rec: bool):
+        record["on"] = rec
+        trainer.run_pass(epoch, T, tokens_before=0)
 
     for w in range(args.warmup):
         one_step(10_000 + w, False)
@@ -338,24 +344,38 @@ def main():
         except Exception:
             traffic = None
 
-    # end to end through the public API: host ids in (pinned), host model out (pinned)
+    # end to end through the public API with host buffers (pinned): ids H2D, model init,
+    # subsampling + training (+ averaging at N > 1), model D2H. N = 1 goes through the
+    # reference-facing C-ABI call cg_train(); N > 1 through api.Session + ReplicaTrainer.
     e2e = None
     if args.e2e_steps > 0:
         ids_pin = torch.from_numpy(host_ids(ids)).pin_memory()
         out0 = torch.empty((vocab.size(), c.dim), dtype=torch.float32).pin_memory()
         out1 = torch.empty((vocab.size() - 1, c.dim), dtype=torch.float32).pin_memory()
-        from paper_1606_07822_b200._lib import CgTrainStats, check, load, ptr
         import ctypes as C
+
+        from paper_1606_07822_b200._lib import CgTrainStats, check, load, ptr
 
         keep: list = []
         desc = api.model_desc(vocab, tree, sel, keep)
         ccfg = cfg.to_c()
         walls = []
         for _ in range(args.e2e_steps):
-            st = CgTrainStats()
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
-            check(load().cg_train(C.byref(ccfg), 0, C.byref(desc), ptr(ids_pin.numpy(), C.c_int32), T,
-                                  ptr(out0.numpy(), C.c_float), ptr(out1.numpy(), C.c_float), C.byref(st)))
+            if world == 1:
+                st = CgTrainStats()
+                check(load().cg_train(C.byref(ccfg), 0, C.byref(desc), ptr(ids_pin.numpy(), C.c_int32), T,
+                                      ptr(out0.numpy(), C.c_float), ptr(out1.numpy(), C.c_float), C.byref(st)))
+            else:
+                s2 = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
+                s2.upload_ids(ids_pin.numpy())
+                rt2 = ReplicaTrainer(lambda e, a, b, base, mult: s2.train_range(e, a, b, base, mult),
+                                     s2.model_tensor(), world, rank, args.sync_words)
+                rt2.run_pass(0, T)
+                m = s2.download()
+                s2.close()
             walls.append(time.perf_counter() - t0)
         e2e_wall = float(np.median(walls))
         if world > 1:
@@ -364,7 +384,8 @@ def main():
             e2e_wall = float(t.item())
         e2e = {"value": float(T) * world / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": int(T * 4),
                "d2h_bytes_per_step": int(out0.numel() * 4 + out1.numel() * 4),
-               "note": "cg_train(): host ids -> device, model init, subsample + train, device -> host model"}
+               "note": ("cg_train()" if world == 1 else "api.Session + ReplicaTrainer") +
+                       ": host ids -> device, model init, subsample + train, device -> host model"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -1,0 +1,113 @@
+"""Multi-replica orchestration (shards, averaging cadence, global-progress estimate)
+on CPU with torch.distributed gloo, world_size 2. The local step is the oracle's
+single-worker trainer (test infrastructure) standing in for the device kernels; the
+expected result is recomputed sequentially in one process."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle_lib as O
+from paper_1606_07822_b200.replicas import ReplicaTrainer, plan_chunks, shard_bounds
+
+V, D = 60, 8
+
+
+def corpus():
+    rng = np.random.default_rng(7)
+    p = 1.0 / np.arange(1, V + 1)
+    ids = rng.choice(V, size=24_000, p=p / p.sum()).astype(np.int32)
+    counts = np.bincount(ids, minlength=V).astype(np.int64)
+    order = np.argsort(-counts, kind="stable")
+    rank = np.empty(V, np.int32)
+    rank[order] = np.arange(V)
+    return rank[ids], counts[order]
+
+
+def local_step_factory(ids, counts, model_np):
+    tree = O.orc_tree(counts)
+    hot, slot = O.orc_select(tree.usage, 7)
+    import ctypes as C
+
+    def step(epoch, a, b, base, mult):
+        cfg = O.OrcConfig(D, 3, 1, 1e-3, 0.025, 1, 1, 7, 10, 11 + epoch)
+        st = O.OrcStats()
+        seg = np.ascontiguousarray(ids[a:b])
+        syn0 = model_np[: V * D].reshape(V, D)
+        syn1 = model_np[V * D:].reshape(V - 1, D)
+        s0 = np.ascontiguousarray(syn0)
+        s1 = np.ascontiguousarray(syn1)
+        O.oracle().orc_train_single(O._p(seg, C.c_int32), seg.size, V, O._p(counts, C.c_int64), int(counts.sum()),
+                                    O._p(tree.off, C.c_int64), O._p(tree.nodes, C.c_int32),
+                                    O._p(tree.turns, C.c_uint8), O._p(hot, C.c_int32), hot.size,
+                                    O._p(slot, C.c_int32), C.byref(cfg), O._p(s0, C.c_float), O._p(s1, C.c_float),
+                                    C.byref(st))
+        syn0[:] = s0
+        syn1[:] = s1
+        return (epoch, a, b, base, mult)
+
+    return step
+
+
+def init_model():
+    s0, s1 = O.orc_init(V, D, 3)
+    return np.concatenate([s0.ravel(), s1.ravel()]).astype(np.float32)
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ids, counts = corpus()
+    a, b = shard_bounds(ids.size, world, rank)
+    model = torch.from_numpy(init_model())
+    rt = ReplicaTrainer(local_step_factory(ids[a:b], counts, model.numpy()), model, world, rank, sync_words=5000)
+    calls = rt.run_pass(0, b - a) + rt.run_pass(1, b - a, tokens_before=b - a)
+    out[rank] = (model.numpy().copy(), calls, rt.syncs)
+    dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_plan_and_shards():
+    assert [(c.begin, c.end) for c in plan_chunks(10, 4)] == [(0, 4), (4, 8), (8, 10)]
+    assert plan_chunks(0, 4) == []
+    bounds = [shard_bounds(10, 3, r) for r in range(3)]
+    assert bounds == [(0, 3), (3, 6), (6, 10)]
+
+
+def test_two_replicas_gloo_average_matches_sequential_simulation():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, start_method="spawn", join=True)
+    m0, calls0, syncs0 = out[0]
+    m1, calls1, _ = out[1]
+    assert np.array_equal(m0, m1)  # replicas agree after every averaging point
+    ids, counts = corpus()
+    n = [shard_bounds(ids.size, world, r) for r in range(world)]
+    # progress estimate: base = world x local tokens before the chunk, mult = world
+    assert calls0[0] == (0, 0, 5000, 0, 2) and calls0[1] == (0, 5000, 10000, 10000, 2)
+    assert calls0[len(plan_chunks(n[0][1] - n[0][0], 5000))][3] == (n[0][1] - n[0][0]) * world
+    assert syncs0 == 2 * len(plan_chunks(n[0][1] - n[0][0], 5000))
+    # sequential simulation of the same schedule
+    models = [init_model() for _ in range(world)]
+    steps = [local_step_factory(ids[a:b], counts, models[r]) for r, (a, b) in enumerate(n)]
+    for epoch in range(2):
+        chunks = [plan_chunks(b - a, 5000) for a, b in n]
+        for i in range(max(len(c) for c in chunks)):
+            for r in range(world):
+                if i < len(chunks[r]):
+                    ch = chunks[r][i]
+                    steps[r](epoch, ch.begin, ch.end, 0, world)
+            avg = (models[0] + models[1]) / 2
+            for r in range(world):
+                models[r][:] = avg
+    np.testing.assert_allclose(m0, models[0], rtol=0, atol=1e-6)
