@@ -263,7 +263,7 @@ def main():
     tree = api.build_huffman_tree(vocab)
     sel = api.select_cached_nodes(tree, args.cache_nodes)
     cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
-                          cache_nodes=args.cache_nodes, seed=c.seed)
+                          cache_nodes=args.cache_nodes, seed=c.seed, mode="hogwild")
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
     sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale)

@@ -7,10 +7,14 @@
 // through the C-ABI (include/cachegram_b200.h); there is no CPU training path.
 //
 // Additions (defaulted, so existing callers compile unchanged):
-//   TrainConfig::mode   TrainMode::Hogwild (default, the throughput path) or
-//                       TrainMode::Deterministic (bit-identical to the reference's
-//                       single-worker run; requires workers == 1).
-//   ConstantSigmoid     a sigmoid functor train_center can ship to the device.
+//   TrainConfig::mode   TrainMode::Auto (default): workers == 1 runs the deterministic
+//                       device mode, bit-identical to the reference's single-worker run
+//                       (the reference is deterministic exactly then); workers > 1 runs
+//                       the Hogwild throughput path on every SM (the reference is Hogwild
+//                       then). TrainMode::Hogwild / ::Deterministic force one or the other.
+//   ConstantSigmoid     a sigmoid functor the device evaluates itself (like SigmoidTable and
+//                       ExactSigmoid); any other SigmoidFn is called back on the host per
+//                       path step while the device does the arithmetic (cg_train_center_cb).
 #pragma once
 
 #include <cstdint>
@@ -30,7 +34,7 @@
 
 namespace cachegram {
 
-enum class TrainMode : std::int32_t { Hogwild = CG_MODE_HOGWILD, Deterministic = CG_MODE_DETERMINISTIC };
+enum class TrainMode : std::int32_t { Hogwild = CG_MODE_HOGWILD, Deterministic = CG_MODE_DETERMINISTIC, Auto = -1 };
 
 struct TrainConfig {
     std::int32_t dim = 100;
@@ -43,7 +47,12 @@ struct TrainConfig {
     std::int32_t cache_nodes = 31;
     std::int32_t flush_interval = 10;
     std::uint64_t seed = 1;
-    TrainMode mode = TrainMode::Hogwild;
+    TrainMode mode = TrainMode::Auto;
+
+    TrainMode resolved_mode() const {
+        if (mode != TrainMode::Auto) return mode;
+        return workers == 1 ? TrainMode::Deterministic : TrainMode::Hogwild;
+    }
 
     void validate() const {
         auto need = [](bool ok, const char* msg) {
@@ -180,33 +189,42 @@ private:
     std::int32_t since_ = 0;
 };
 
-// One skip-gram/HS update for a center word (trainer.hpp:147-175), executed by the
-// deterministic device kernel. SigmoidFn must be SigmoidTable, ExactSigmoid or
-// ConstantSigmoid (functors the device can evaluate). `hidden` is unused: the
-// device keeps the hidden accumulator in shared memory.
+// One skip-gram/HS update for a center word (trainer.hpp:147-175) on the device.
+// SigmoidTable, ExactSigmoid and ConstantSigmoid are evaluated on the device; any other
+// functor (e.g. a test's counting lambda) is called on the host once per path step, in
+// path order, while the device computes the dot products and applies the updates.
+// `hidden` is unused: the device keeps the hidden accumulator in shared memory.
 template <typename SigmoidFn>
 inline void train_center(std::int32_t center, std::span<const std::int32_t> sentence, std::size_t center_pos,
                          std::int32_t half_window, Model& model, const HuffmanTree& tree,
                          const CacheSelection& selection, NodeCache& cache, float alpha, float* hidden,
                          const SigmoidFn& sigmoid, std::int64_t* sigmoid_calls = nullptr) {
-    static_assert(trainer_detail::kDeviceSigmoid<SigmoidFn>,
-                  "train_center runs on the GPU: use SigmoidTable, ExactSigmoid or ConstantSigmoid");
     (void)hidden;
-    std::int32_t mode = 0;
-    float konst = 0.0f;
-    if constexpr (std::is_same_v<SigmoidFn, ExactSigmoid>) mode = 1;
-    if constexpr (std::is_same_v<SigmoidFn, ConstantSigmoid>) {
-        mode = 2;
-        konst = sigmoid.value;
-    }
     const trainer_detail::TreeArrays ta(tree);
     std::vector<std::int32_t> slot_of(static_cast<std::size_t>(selection.inner_node_count()));
     for (std::int32_t n = 0; n < selection.inner_node_count(); ++n) slot_of[static_cast<std::size_t>(n)] = selection.slot_of(n);
-    trainer_detail::check(cg_train_center(
-        center, sentence.data(), static_cast<std::int64_t>(sentence.size()), static_cast<std::int64_t>(center_pos),
-        half_window, model.vocab_size(), model.dim(), model.input_matrix().data(), model.weight_matrix().data(),
-        ta.off.data(), ta.node.data(), ta.turn.data(), slot_of.data(), selection.size(), cache.work_data(),
-        cache.snap_data(), cache.flag_data(), alpha, mode, konst, sigmoid_calls));
+    if constexpr (trainer_detail::kDeviceSigmoid<SigmoidFn>) {
+        std::int32_t mode = 0;
+        float konst = 0.0f;
+        if constexpr (std::is_same_v<SigmoidFn, ExactSigmoid>) mode = 1;
+        if constexpr (std::is_same_v<SigmoidFn, ConstantSigmoid>) {
+            mode = 2;
+            konst = sigmoid.value;
+        }
+        trainer_detail::check(cg_train_center(
+            center, sentence.data(), static_cast<std::int64_t>(sentence.size()), static_cast<std::int64_t>(center_pos),
+            half_window, model.vocab_size(), model.dim(), model.input_matrix().data(), model.weight_matrix().data(),
+            ta.off.data(), ta.node.data(), ta.turn.data(), slot_of.data(), selection.size(), cache.work_data(),
+            cache.snap_data(), cache.flag_data(), alpha, mode, konst, sigmoid_calls));
+    } else {
+        auto trampoline = [](float x, void* ctx) -> float { return (*static_cast<const SigmoidFn*>(ctx))(x); };
+        trainer_detail::check(cg_train_center_cb(
+            center, sentence.data(), static_cast<std::int64_t>(sentence.size()), static_cast<std::int64_t>(center_pos),
+            half_window, model.vocab_size(), model.dim(), model.input_matrix().data(), model.weight_matrix().data(),
+            ta.off.data(), ta.node.data(), ta.turn.data(), slot_of.data(), selection.size(), cache.work_data(),
+            cache.snap_data(), cache.flag_data(), alpha, trampoline,
+            const_cast<void*>(static_cast<const void*>(&sigmoid)), sigmoid_calls));
+    }
 }
 
 // cachegram::train (trainer.hpp:254-316) on the GPU.
@@ -216,7 +234,8 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
     if (vocab.size() != tree.leaf_count()) throw std::invalid_argument("vocabulary and tree sizes disagree");
     if (selection.inner_node_count() != tree.inner_count())
         throw std::invalid_argument("cache selection was built from a different tree");
-    if (config.mode == TrainMode::Deterministic && config.workers != 1)
+    const TrainMode mode = config.resolved_mode();
+    if (mode == TrainMode::Deterministic && config.workers != 1)
         throw std::invalid_argument("deterministic mode replays the single-worker stream: set workers = 1");
 
     const std::vector<std::int32_t> ids = read_id_stream(corpus_path, vocab);  // IoError if unreadable
@@ -241,7 +260,7 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
 
     Model model(vocab.size(), config.dim);
     cg_train_stats st{};
-    trainer_detail::check(cg_train(&c, static_cast<std::int32_t>(config.mode), &m, ids.data(),
+    trainer_detail::check(cg_train(&c, static_cast<std::int32_t>(mode), &m, ids.data(),
                                    static_cast<std::int64_t>(ids.size()), model.input_matrix().data(),
                                    model.weight_matrix().data(), &st));
     if (stats) {

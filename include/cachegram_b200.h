@@ -142,6 +142,17 @@ CG_API int cg_train_center(int32_t center, const int32_t* sentence, int64_t sent
                     const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
                     const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
                     uint8_t* cache_flag, float alpha, int32_t sigmoid_mode, float sig_const, int64_t* sigmoid_calls);
+/* train_center with an arbitrary host sigmoid functor (the reference's SigmoidFn template
+ * parameter, e.g. its tests' counting lambdas): per pair the device computes the L exact
+ * dot products, fn maps each through the sigmoid on the host (in path order, one call
+ * per step like the reference), and the device applies the updates. Same cache contract
+ * as cg_train_center. */
+typedef float (*cg_sigmoid_fn)(float x, void* ctx);
+CG_API int cg_train_center_cb(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
+                              int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
+                              const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
+                              const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
+                              uint8_t* cache_flag, float alpha, cg_sigmoid_fn fn, void* ctx, int64_t* sigmoid_calls);
 /* NodeCache::flush (trainer.hpp:110-124) on the device: syn1[hot_nodes[s]] += work - snap
  * for every acquired slot, then clears the flags. */
 CG_API int cg_cache_flush(int32_t vocab_size, int32_t dim, float* syn1, const int32_t* hot_nodes, int32_t hot_count,

@@ -89,6 +89,7 @@ class CgTuning(C.Structure):
 
 P = C.POINTER
 vp = C.c_void_p
+SIGMOID_FN = C.CFUNCTYPE(C.c_float, C.c_float, C.c_void_p)
 # name -> (restype, argtypes); mirrors include/cachegram_b200.h
 SIGNATURES = {
     "cg_abi_version": (C.c_int, []),
@@ -114,6 +115,10 @@ SIGNATURES = {
                                   P(C.c_float), P(C.c_float), P(C.c_int64), P(C.c_int32), P(C.c_uint8),
                                   P(C.c_int32), C.c_int32, P(C.c_float), P(C.c_float), P(C.c_uint8), C.c_float,
                                   C.c_int32, C.c_float, P(C.c_int64)]),
+    "cg_train_center_cb": (C.c_int, [C.c_int32, P(C.c_int32), C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                     P(C.c_float), P(C.c_float), P(C.c_int64), P(C.c_int32), P(C.c_uint8),
+                                     P(C.c_int32), C.c_int32, P(C.c_float), P(C.c_float), P(C.c_uint8), C.c_float,
+                                     C.c_void_p, C.c_void_p, P(C.c_int64)]),
     "cg_cache_flush": (C.c_int, [C.c_int32, C.c_int32, P(C.c_float), P(C.c_int32), C.c_int32, P(C.c_float),
                                  P(C.c_float), P(C.c_uint8)]),
     "cg_session_create": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), C.c_int32, vp, P(vp)]),

@@ -22,10 +22,18 @@ from ._lib import CgConfig, CgEpochStats, CgModelDesc, CgTrainStats, check, load
 MODES = {"hogwild": _lib.CG_MODE_HOGWILD, "deterministic": _lib.CG_MODE_DETERMINISTIC}
 
 
+def resolve_mode(config: "TrainConfig") -> str:
+    """"auto" (default): workers == 1 -> the reference's deterministic single-worker
+    semantics (bit-identical), workers > 1 -> Hogwild on every SM."""
+    if config.mode != "auto":
+        return config.mode
+    return "deterministic" if config.workers == 1 else "hogwild"
+
+
 # --------------------------------------------------------------------------- config
 @dataclass
 class TrainConfig:
-    """trainer.hpp:25-48 (+ ``mode``: "hogwild" (default) or "deterministic")."""
+    """trainer.hpp:25-48 (+ ``mode``: "auto" (default), "hogwild" or "deterministic")."""
     dim: int = 100
     window: int = 5
     min_count: int = 5
@@ -36,7 +44,7 @@ class TrainConfig:
     cache_nodes: int = 31
     flush_interval: int = 10
     seed: int = 1
-    mode: str = "hogwild"
+    mode: str = "auto"
 
     def validate(self) -> None:
         for ok, msg in (
@@ -52,7 +60,7 @@ class TrainConfig:
         ):
             if not ok:
                 raise ValueError(msg)
-        if self.mode not in MODES:
+        if self.mode not in MODES and self.mode != "auto":
             raise ValueError(f"unknown training mode {self.mode!r}")
 
     def to_c(self) -> CgConfig:
@@ -335,9 +343,24 @@ class NodeCache:
 
 def train_center(center: int, sentence: Sequence[int], center_pos: int, half_window: int, model: Model,
                  tree: HuffmanTree, selection: CacheSelection, cache: NodeCache, alpha: float,
-                 sigmoid: str | float = "table") -> int:
-    """trainer.hpp:147-175 on the device. sigmoid: "table", "exact" or a constant.
-    Returns the number of sigmoid evaluations (= pairs x path length)."""
+                 sigmoid="table") -> int:
+    """trainer.hpp:147-175 on the device. sigmoid: "table", "exact", a constant (all
+    evaluated on the device) or any callable float -> float (called on the host once per
+    path step, in path order, like the reference's SigmoidFn). Returns the number of
+    sigmoid evaluations (= pairs x path length)."""
+    if callable(sigmoid):
+        sent = np.ascontiguousarray(np.asarray(sentence, np.int32))
+        slot = np.ascontiguousarray(selection.slot, np.int32)
+        cb = _lib.SIGMOID_FN(lambda x, _ctx: float(sigmoid(x)))
+        calls = C.c_int64()
+        check(load().cg_train_center_cb(
+            int(center), ptr(sent, C.c_int32), sent.size, int(center_pos), int(half_window), model.vocab_size(),
+            model.dim(), ptr(model.syn0, C.c_float), ptr(model.syn1, C.c_float), ptr(tree.offsets, C.c_int64),
+            ptr(tree.nodes, C.c_int32), ptr(tree.turns, C.c_uint8),
+            ptr(slot, C.c_int32) if selection.size() else None, selection.size(), ptr(cache.work, C.c_float),
+            ptr(cache.snap, C.c_float), ptr(cache.flag, C.c_uint8), float(alpha), C.cast(cb, C.c_void_p), None,
+            C.byref(calls)))
+        return calls.value
     if isinstance(sigmoid, str):
         mode, const = {"table": 0, "exact": 1}[sigmoid], 0.0
     else:
@@ -363,7 +386,8 @@ def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelectio
     in-vocabulary int32 id stream."""
     config.validate()
     _check_consistency(vocab, tree, selection)
-    if config.mode == "deterministic" and config.workers != 1:
+    mode = resolve_mode(config)
+    if mode == "deterministic" and config.workers != 1:
         raise ValueError("deterministic mode replays the single-worker stream: set workers = 1")
     if isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__"):
         ids = read_id_stream(str(corpus), vocab)
@@ -374,7 +398,7 @@ def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelectio
     cfg = config.to_c()
     m = Model(vocab.size(), config.dim)
     st = CgTrainStats()
-    check(load().cg_train(C.byref(cfg), MODES[config.mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
+    check(load().cg_train(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
                           ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
     if stats is not None:
         stats.words_processed = st.words_processed
@@ -400,7 +424,7 @@ class Session:
         desc = model_desc(vocab, tree, selection, self._keep)
         cfg = config.to_c()
         self._h = C.c_void_p()
-        check(load().cg_session_create(C.byref(cfg), MODES[config.mode], C.byref(desc), device,
+        check(load().cg_session_create(C.byref(cfg), MODES[resolve_mode(config)], C.byref(desc), device,
                                        C.c_void_p(stream) if stream else None, C.byref(self._h)))
         self.n_ids = 0
 

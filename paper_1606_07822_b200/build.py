@@ -83,10 +83,26 @@ def build_cpp_dropin_test() -> Path:
     return out
 
 
+def build_reference_suites() -> None:
+    """The reference's own unit tests against the drop-in headers (needs /root/reference)."""
+    script = ROOT / "tests" / "cpp" / "build_reftests.sh"
+    if not Path("/root/reference/proj/tests").exists():
+        return
+    out = ROOT / "tests" / "cpp" / "_reftests" / "trainer_test"
+    deps = [OUT, ROOT / "tests" / "cpp" / "gtest_shim" / "gtest" / "gtest.h", *(ROOT / "include").rglob("*.h*")]
+    if out.exists() and all(d.stat().st_mtime < out.stat().st_mtime for d in deps):
+        return
+    res = subprocess.run(["sh", str(script)], capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("reference test suites failed to build against the drop-in headers")
+
+
 def build_all(force: bool = False) -> None:
     build_library(force=force)
     build_oracle()
     build_cpp_dropin_test()
+    build_reference_suites()
 
 
 if __name__ == "__main__":

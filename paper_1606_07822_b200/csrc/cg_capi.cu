@@ -729,56 +729,58 @@ int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, con
 }
 
 // ---- kernel-level entries ---------------------------------------------------------
-int cg_train_center(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
-                    int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
-                    const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
-                    const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
-                    uint8_t* cache_flag, float alpha, int32_t sigmoid_mode, float sig_const, int64_t* sigmoid_calls) {
-    return guarded([&] {
-        if (vocab_size < 2 || dim < 1) invalid("bad model geometry");
-        if (center < 0 || center >= vocab_size) invalid("center out of range");
-        if (center_pos < 0 || center_pos >= sentence_len) invalid("center position out of range");
-        if (half_window < 0) invalid("half window must be >= 0");
-        if (hot_count > 0 && (!slot_of || !cache_work || !cache_snap || !cache_flag)) invalid("cache arrays missing");
+}  // extern "C"
+
+namespace {
+// Device copies of one train_center call's operands (kernel-level entries; tests).
+struct CenterCall {
+    DevBuf<float> d0, d1, work, snap, sig, buf;
+    DevBuf<int64_t> off;
+    DevBuf<int32_t> node, slot, sent, acq, nacq;
+    DevBuf<uint8_t> turn, flag;
+    DevBuf<unsigned long long> evals;
+    cgk::DetModel m{};
+    size_t n0 = 0, n1 = 0;
+    int32_t hot = 0, dim = 0;
+
+    void up(const int32_t* sentence, int64_t len, int32_t V, int32_t D, float* syn0, float* syn1,
+            const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns, const int32_t* slot_of,
+            int32_t hot_count, float* cache_work, float* cache_snap, uint8_t* cache_flag) {
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
             cudaGetLastError();
             throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
         }
-        cudaStream_t st = nullptr;
-        const size_t n0 = static_cast<size_t>(vocab_size) * dim, n1 = static_cast<size_t>(vocab_size - 1) * dim;
-        const int64_t steps = path_offsets[vocab_size];
-        DevBuf<float> d0, d1, work, snap, sig;
-        DevBuf<int64_t> off;
-        DevBuf<int32_t> node, slot, sent, acq, nacq;
-        DevBuf<uint8_t> turn, flag;
-        DevBuf<unsigned long long> evals;
-        d0.upload(syn0, n0, st);
-        d1.upload(syn1, n1, st);
-        off.upload(path_offsets, static_cast<size_t>(vocab_size) + 1, st);
-        node.upload(path_nodes, static_cast<size_t>(steps), st);
-        turn.upload(path_turns, static_cast<size_t>(steps), st);
-        sent.upload(sentence, static_cast<size_t>(sentence_len), st);
+        hot = hot_count;
+        dim = D;
+        n0 = static_cast<size_t>(V) * D;
+        n1 = static_cast<size_t>(V - 1) * D;
+        const int64_t steps = path_offsets[V];
+        d0.upload(syn0, n0, nullptr);
+        d1.upload(syn1, n1, nullptr);
+        off.upload(path_offsets, static_cast<size_t>(V) + 1, nullptr);
+        node.upload(path_nodes, static_cast<size_t>(steps), nullptr);
+        turn.upload(path_turns, static_cast<size_t>(steps), nullptr);
+        sent.upload(sentence, static_cast<size_t>(len), nullptr);
         const cachegram::SigmoidTable table;
-        sig.upload(table.data(), 1000, st);
+        sig.upload(table.data(), 1000, nullptr);
         int32_t zero = 0;
-        nacq.upload(&zero, 1, st);
+        nacq.upload(&zero, 1, nullptr);
         evals.alloc(1);
-        cgk::DetModel m{};
         m.syn0 = d0.p;
         m.syn1 = d1.p;
-        m.dim = dim;
-        m.vocab = vocab_size;
+        m.dim = D;
+        m.vocab = V;
         m.path_off = off.p;
         m.path_node = node.p;
         m.path_turn = turn.p;
         m.sigmoid = sig.p;
         m.sig_scale = host_sig_scale();
         if (hot_count > 0) {
-            slot.upload(slot_of, static_cast<size_t>(vocab_size - 1), st);
-            work.upload(cache_work, static_cast<size_t>(hot_count) * dim, st);
-            snap.upload(cache_snap, static_cast<size_t>(hot_count) * dim, st);
-            flag.upload(cache_flag, static_cast<size_t>(hot_count), st);
+            slot.upload(slot_of, static_cast<size_t>(V - 1), nullptr);
+            work.upload(cache_work, static_cast<size_t>(hot_count) * D, nullptr);
+            snap.upload(cache_snap, static_cast<size_t>(hot_count) * D, nullptr);
+            flag.upload(cache_flag, static_cast<size_t>(hot_count), nullptr);
             acq.alloc(static_cast<size_t>(hot_count));
             m.slot_of = slot.p;
             m.hot_count = hot_count;
@@ -787,29 +789,93 @@ int cg_train_center(int32_t center, const int32_t* sentence, int64_t sentence_le
             m.cache_flag = flag.p;
             m.acquired = acq.p;
         }
+    }
+    void down(float* syn0, float* syn1, float* cache_work, float* cache_snap, uint8_t* cache_flag) {
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpy(syn0, d0.p, n0 * 4, cudaMemcpyDeviceToHost));
+        CG_CUDA(cudaMemcpy(syn1, d1.p, n1 * 4, cudaMemcpyDeviceToHost));
+        if (hot > 0) {
+            CG_CUDA(cudaMemcpy(cache_work, work.p, static_cast<size_t>(hot) * dim * 4, cudaMemcpyDeviceToHost));
+            CG_CUDA(cudaMemcpy(cache_snap, snap.p, static_cast<size_t>(hot) * dim * 4, cudaMemcpyDeviceToHost));
+            CG_CUDA(cudaMemcpy(cache_flag, flag.p, static_cast<size_t>(hot), cudaMemcpyDeviceToHost));
+        }
+    }
+};
+
+void check_center_args(int32_t center, int64_t sentence_len, int64_t center_pos, int32_t half_window,
+                       int32_t vocab_size, int32_t dim, const int32_t* slot_of, int32_t hot_count, float* cache_work,
+                       float* cache_snap, uint8_t* cache_flag) {
+    if (vocab_size < 2 || dim < 1) invalid("bad model geometry");
+    if (center < 0 || center >= vocab_size) invalid("center out of range");
+    if (center_pos < 0 || center_pos >= sentence_len) invalid("center position out of range");
+    if (half_window < 0) invalid("half window must be >= 0");
+    if (hot_count > 0 && (!slot_of || !cache_work || !cache_snap || !cache_flag)) invalid("cache arrays missing");
+}
+}  // namespace
+
+extern "C" {
+
+int cg_train_center(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
+                    int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
+                    const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
+                    const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
+                    uint8_t* cache_flag, float alpha, int32_t sigmoid_mode, float sig_const, int64_t* sigmoid_calls) {
+    return guarded([&] {
+        check_center_args(center, sentence_len, center_pos, half_window, vocab_size, dim, slot_of, hot_count,
+                          cache_work, cache_snap, cache_flag);
+        if (sigmoid_mode < 0 || sigmoid_mode > 2) invalid("sigmoid_mode must be 0, 1 or 2");
+        CenterCall cc;
+        cc.up(sentence, sentence_len, vocab_size, dim, syn0, syn1, path_offsets, path_nodes, path_turns, slot_of,
+              hot_count, cache_work, cache_snap, cache_flag);
         cgk::DetCenter c{};
         c.center = center;
-        c.sentence = sent.p;
+        c.sentence = cc.sent.p;
         c.len = sentence_len;
         c.pos = center_pos;
         c.half_window = half_window;
         c.alpha = alpha;
         c.sigmoid_mode = sigmoid_mode;
         c.sig_const = sig_const;
-        c.n_acquired = nacq.p;
-        c.evals = evals.p;
-        cgk::launch_det_center(m, c, st);
-        CG_CUDA(cudaGetLastError());
-        CG_CUDA(cudaMemcpy(syn0, d0.p, n0 * 4, cudaMemcpyDeviceToHost));
-        CG_CUDA(cudaMemcpy(syn1, d1.p, n1 * 4, cudaMemcpyDeviceToHost));
-        if (hot_count > 0) {
-            CG_CUDA(cudaMemcpy(cache_work, work.p, static_cast<size_t>(hot_count) * dim * 4, cudaMemcpyDeviceToHost));
-            CG_CUDA(cudaMemcpy(cache_snap, snap.p, static_cast<size_t>(hot_count) * dim * 4, cudaMemcpyDeviceToHost));
-            CG_CUDA(cudaMemcpy(cache_flag, flag.p, static_cast<size_t>(hot_count), cudaMemcpyDeviceToHost));
-        }
+        c.n_acquired = cc.nacq.p;
+        c.evals = cc.evals.p;
+        cgk::launch_det_center(cc.m, c, nullptr);
+        cc.down(syn0, syn1, cache_work, cache_snap, cache_flag);
         unsigned long long e = 0;
-        CG_CUDA(cudaMemcpy(&e, evals.p, sizeof e, cudaMemcpyDeviceToHost));
+        CG_CUDA(cudaMemcpy(&e, cc.evals.p, sizeof e, cudaMemcpyDeviceToHost));
         if (sigmoid_calls) *sigmoid_calls = static_cast<int64_t>(e);
+    });
+}
+
+int cg_train_center_cb(int32_t center, const int32_t* sentence, int64_t sentence_len, int64_t center_pos,
+                       int32_t half_window, int32_t vocab_size, int32_t dim, float* syn0, float* syn1,
+                       const int64_t* path_offsets, const int32_t* path_nodes, const uint8_t* path_turns,
+                       const int32_t* slot_of, int32_t hot_count, float* cache_work, float* cache_snap,
+                       uint8_t* cache_flag, float alpha, cg_sigmoid_fn fn, void* ctx, int64_t* sigmoid_calls) {
+    return guarded([&] {
+        check_center_args(center, sentence_len, center_pos, half_window, vocab_size, dim, slot_of, hot_count,
+                          cache_work, cache_snap, cache_flag);
+        if (!fn) invalid("null sigmoid callback");
+        CenterCall cc;
+        cc.up(sentence, sentence_len, vocab_size, dim, syn0, syn1, path_offsets, path_nodes, path_turns, slot_of,
+              hot_count, cache_work, cache_snap, cache_flag);
+        const int L = static_cast<int>(path_offsets[center + 1] - path_offsets[center]);
+        cc.buf.alloc(static_cast<size_t>(L));
+        std::vector<float> host(static_cast<size_t>(L));
+        const int64_t lo = center_pos >= half_window ? center_pos - half_window : 0;
+        const int64_t hi = std::min(sentence_len - 1, center_pos + half_window);
+        int64_t calls = 0;
+        for (int64_t pos = lo; pos <= hi; ++pos) {
+            if (pos == center_pos) continue;
+            cgk::launch_det_pair(cc.m, center, sentence[pos], alpha, 0, cc.buf.p, cc.nacq.p, nullptr);
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaMemcpy(host.data(), cc.buf.p, host.size() * 4, cudaMemcpyDeviceToHost));
+            for (float& x : host) x = fn(x, ctx);  // path order, one call per step
+            calls += L;
+            CG_CUDA(cudaMemcpy(cc.buf.p, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
+            cgk::launch_det_pair(cc.m, center, sentence[pos], alpha, 1, cc.buf.p, cc.nacq.p, nullptr);
+        }
+        cc.down(syn0, syn1, cache_work, cache_snap, cache_flag);
+        if (sigmoid_calls) *sigmoid_calls = calls;
     });
 }
 

@@ -214,6 +214,74 @@ __global__ void det_center_kernel(DetModel m, DetCenter c) {
     }
 }
 
+// Host-callback sigmoid (train_center with an arbitrary SigmoidFn functor): one pair in
+// two phases. Phase 0 acquires the path's hot rows (first touch, trainer.hpp:161-165)
+// and writes the L exact sequential dot products; the host maps them through the
+// functor; phase 1 applies g = ((1 - turn) - f) * alpha, h += g*u, u += g*v, v += h with
+// the same rounding as det_center_warp. Exact: the dots of one pair do not depend on
+// the pair's own updates (distinct rows, fixed context row).
+__global__ void det_pair_kernel(DetModel m, int32_t center, int32_t context, float alpha, int phase, float* buf,
+                                int32_t* n_acquired) {
+    DetSmem sm = carve(m.dim);
+    const int lane = threadIdx.x & 31;
+    const int D = m.dim;
+    const int64_t p0 = m.path_off[center];
+    const int L = static_cast<int>(m.path_off[center + 1] - p0);
+    float* v = m.syn0 + static_cast<size_t>(context) * D;
+    int32_t n_acq = *n_acquired;
+    for (int d = lane; d < D; d += 32) {
+        sm.vbuf[d] = v[d];
+        sm.hbuf[d] = 0.0f;
+    }
+    __syncwarp();
+    for (int j0 = 0; j0 < L; j0 += 32) {
+        const int j = j0 + lane;
+        float* u = nullptr;
+        bool fresh = false;
+        if (j < L) {
+            const int32_t node = m.path_node[p0 + j];
+            const int32_t slot = m.slot_of ? m.slot_of[node] : -1;
+            float* shared_row = m.syn1 + static_cast<size_t>(node) * D;
+            if (phase == 0) {
+                u = slot >= 0 ? det_acquire(m, slot, shared_row, fresh) : shared_row;
+                float acc = 0.0f;
+                for (int d = 0; d < D; ++d) acc = __fadd_rn(acc, __fmul_rn(sm.vbuf[d], u[d]));
+                buf[j] = acc;
+            } else {
+                u = slot >= 0 ? m.cache_work + static_cast<size_t>(slot) * D : shared_row;
+            }
+        }
+        if (phase == 0) {
+            const unsigned fm = __ballot_sync(kFull, fresh);
+            if (fresh) m.acquired[n_acq + __popc(fm & ((1u << lane) - 1u))] = m.slot_of[m.path_node[p0 + j]];
+            n_acq += __popc(fm);
+            continue;
+        }
+        const float g = j < L ? __fmul_rn(__fsub_rn(__fsub_rn(1.0f, static_cast<float>(m.path_turn[p0 + j])), buf[j]),
+                                          alpha)
+                              : 0.0f;
+        sm.gbuf[lane] = g;
+        sm.ubuf[lane] = u;
+        __syncwarp();
+        const int nj = min(32, L - j0);
+        for (int d = lane; d < D; d += 32) {
+            const float vd = sm.vbuf[d];
+            float h = sm.hbuf[d];
+            for (int k = 0; k < nj; ++k) {
+                float* ur = sm.ubuf[k];
+                const float uo = ur[d];
+                h = __fadd_rn(h, __fmul_rn(sm.gbuf[k], uo));
+                ur[d] = __fadd_rn(uo, __fmul_rn(sm.gbuf[k], vd));
+            }
+            sm.hbuf[d] = h;
+        }
+        __syncwarp();
+    }
+    if (phase == 1)
+        for (int d = lane; d < D; d += 32) v[d] = __fadd_rn(sm.vbuf[d], sm.hbuf[d]);
+    if (lane == 0) *n_acquired = n_acq;
+}
+
 // Flush driven by flags (order-free: every acquired slot touches a distinct row).
 __global__ void det_flush_flags_kernel(DetModel m) {
     const int lane = threadIdx.x & 31;
@@ -246,5 +314,12 @@ void launch_det_center(const DetModel& m, const DetCenter& c, cudaStream_t s) {
 }
 
 void launch_det_flush_flags(const DetModel& m, cudaStream_t s) { det_flush_flags_kernel<<<1, 32, 0, s>>>(m); }
+
+void launch_det_pair(const DetModel& m, int32_t center, int32_t context, float alpha, int phase, float* buf,
+                     int32_t* n_acquired, cudaStream_t s) {
+    const size_t smem = det_smem_bytes(m.dim);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(det_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    det_pair_kernel<<<1, 32, smem, s>>>(m, center, context, alpha, phase, buf, n_acquired);
+}
 
 }  // namespace cgk

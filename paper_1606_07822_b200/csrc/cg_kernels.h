@@ -65,6 +65,10 @@ struct DetCenter {
 };
 void launch_det_center(const DetModel& m, const DetCenter& c, cudaStream_t s);
 void launch_det_flush_flags(const DetModel& m, cudaStream_t s);
+// One (center, context) pair with a host-evaluated sigmoid: phase 0 writes the L dots
+// into buf, phase 1 reads the L sigmoid values from buf and applies the updates.
+void launch_det_pair(const DetModel& m, int32_t center, int32_t context, float alpha, int phase, float* buf,
+                     int32_t* n_acquired, cudaStream_t s);
 
 // ---------------- throughput mode: subsampling + pair generation (K3) ---------
 constexpr int kSubTile = 2048;  // tokens per subsampling block (256 threads x 8)

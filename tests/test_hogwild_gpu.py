@@ -29,7 +29,8 @@ def c1():
 def test_hogwild_covers_stream_and_matches_pair_distribution():
     c, vocab, ids = c1()
     tree, sel = setup(vocab)
-    cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1, seed=1)
+    cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1, seed=1,
+                          mode="hogwild")
     s = api.Session(vocab, tree, sel, cfg)
     s.upload_ids(ids)
     e = s.train_range(0, 0, ids.size, 0, 1)
@@ -51,7 +52,7 @@ def test_hogwild_covers_stream_and_matches_pair_distribution():
 def test_hogwild_multiple_ranges_cover_stream():
     c, vocab, ids = c1()
     tree, sel = setup(vocab, 0)
-    cfg = api.TrainConfig(dim=16, window=3, min_count=1, sample=0.0, iterations=1, seed=3)
+    cfg = api.TrainConfig(dim=16, window=3, min_count=1, sample=0.0, iterations=1, seed=3, mode="hogwild")
     s = api.Session(vocab, tree, sel, cfg)
     s.upload_ids(ids)
     cuts = [0, 12345, 500000, ids.size]
@@ -78,7 +79,7 @@ def test_hogwild_loss_within_2pct_of_reference_c1(k):
                flush_interval=10, seed=1)
     ref0, ref1, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
     ref_loss = _loss(api.Model(vocab.size(), c.dim, ref0, ref1), tree, vocab, ids, c)
-    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg))
+    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg, mode="hogwild"))
     gpu_loss = _loss(m, tree, vocab, ids, c)
     init = api.init_model(vocab.size(), c.dim, 1)
     init_loss = _loss(init, tree, vocab, ids, c)
@@ -110,7 +111,7 @@ def test_hogwild_planted_cluster_recall_matches_reference():
     cfg = dict(dim=cc.dim, window=cc.window, min_count=5, sample=cc.sample, iterations=3, cache_nodes=31,
                flush_interval=10, seed=3)
     r0, _, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
-    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg))
+    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg, mode="hogwild"))
     cluster = cluster_of[vocab.raw_of_id]
     sample = np.arange(0, vocab.size(), 3)
     r_ref = recall_at_10(r0, cluster, sample)

@@ -70,7 +70,7 @@ def main():
         sel = api.select_cached_nodes(tree, a.k)
         cfg = dict(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=c.iterations,
                    cache_nodes=a.k, flush_interval=10, seed=c.seed)
-        gpu = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg))
+        gpu = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg, mode="hogwild"))
         with tempfile.TemporaryDirectory() as d:
             Oref, h, path, n = bench.reference_sample(c, vocab, ids, len(ids), d)
             r0, r1, words, wall = Oref.ref_train(h, path, cfg, workers=threads)

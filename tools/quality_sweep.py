@@ -70,7 +70,7 @@ def main():
     for g in grids[a.grid]:
         k = g.get("k", a.k)
         sel = api.select_cached_nodes(tree, k)
-        cfg = api.TrainConfig(**dict(cfgd, cache_nodes=k))
+        cfg = api.TrainConfig(**dict(cfgd, cache_nodes=k), mode="hogwild")
         s = api.Session(vocab, tree, sel, cfg)
         s.tune(g.get("blocks", 0), g.get("warps", 0), g.get("cpw", 0), -1, g.get("cold", 0), g.get("scale", 0.0),
                g.get("flush", 0), g.get("probe", 0))
