@@ -206,8 +206,11 @@ typedef struct cg_tuning {
     int32_t centers_per_warp; /* 0 = 8: centers a warp trains between block-cache flushes */
     int32_t smem_cache_rows;  /* < 0 = min(K, what fits); hot rows held in the block cache */
     int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
-    float hot_flush_scale;    /* 0 = 1/blocks (model averaging of the per-CTA hot-row replicas) */
+    float hot_flush_scale;    /* 0 = per-row 1/E[#CTAs contributing per flush] (averaging of overlapping
+                                 CTA replicas); > 0 = this multiplier for every cached row */
     int32_t flush_centers;    /* 0 = 64: centers merged into a CTA's cache between flushes */
+    int32_t min_cache_rows;   /* 0 = default (at least the top 31 rows are cached); < 0 = honour K exactly,
+                                 even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
                                  context-row updates, bit 2 skip cache merges */
 } cg_tuning;

@@ -455,9 +455,10 @@ class Session:
                                           ptr(np.ascontiguousarray(model.syn1), C.c_float)))
 
     def tune(self, blocks: int = 0, warps: int = 0, centers_per_warp: int = 0, cache_rows: int = -1,
-             cold_update: int = 0, hot_flush_scale: float = 0.0, flush_centers: int = 0, probe: int = 0) -> None:
+             cold_update: int = 0, hot_flush_scale: float = 0.0, flush_centers: int = 0, min_cache_rows: int = 0,
+             probe: int = 0) -> None:
         t = _lib.CgTuning(blocks, warps, centers_per_warp, cache_rows, cold_update, hot_flush_scale, flush_centers,
-                          probe)
+                          min_cache_rows, probe)
         check(load().cg_session_tune(self._h, C.byref(t)))
 
     def train_range(self, epoch: int, begin: int, end: int, progress_base: int = 0,

@@ -5,6 +5,7 @@
 // CUDA kernel (cg_det.cu, cg_hogwild.cu). There is no CPU training fallback.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -185,8 +186,11 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0, 0};
-    int32_t cached_rows = 0;  // hogwild: hot rows within the kernel's private prefix depth
+    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0, 0, 0};
+    int32_t cached_rows = 0;  // hogwild: rows [0, cached_rows) of syn1 are eligible for the CTA cache
+    std::vector<double> row_share;  // hogwild: usage share (of the root's) of the cache-eligible rows
+    DevBuf<float> row_scale;
+    int scale_blocks = -1, scale_flush = -1, scale_rows = -1;
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -441,6 +445,9 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                     placed[static_cast<size_t>(n)] = 1;
                 }
             }
+            // The GPU always caches at least the top kMinCachedRows rows: uncached, the
+            // top-of-tree rows see ~10^3 concurrent stale updates and training diverges
+            // (DESIGN.md 3). Rows beyond the caller's selection follow in usage order.
             s->cached_rows = static_cast<int32_t>(s->node_of_row.size());
             std::vector<int32_t> rest;
             for (int32_t n = 0; n < V - 1; ++n)
@@ -450,6 +457,13 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                     return md->node_usage[a] > md->node_usage[b];
                 });
             s->node_of_row.insert(s->node_of_row.end(), rest.begin(), rest.end());
+            constexpr int32_t kMinCachedRows = 31;
+            s->cached_rows = std::max(s->cached_rows, std::min(kMinCachedRows, V - 1));
+            if (md->node_usage) {
+                const double root = static_cast<double>(md->node_usage[V - 2]);
+                for (int32_t r = 0; r < s->cached_rows; ++r)
+                    s->row_share.push_back(static_cast<double>(md->node_usage[s->node_of_row[static_cast<size_t>(r)]]) / root);
+            }
             s->row_of_node.assign(static_cast<size_t>(V - 1), 0);
             for (int32_t r = 0; r < V - 1; ++r) s->row_of_node[static_cast<size_t>(s->node_of_row[static_cast<size_t>(r)])] = r;
             std::vector<int32_t> off(static_cast<size_t>(V) + 1), code(static_cast<size_t>(steps));
@@ -650,16 +664,37 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
             h.counters = s->counters.p;
             h.cold_store = s->tune.cold_update;
+            const int32_t want_rows = s->tune.min_cache_rows < 0 ? s->K : s->cached_rows;
             h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 64;
             h.dummy_row = s->V - 1;
             h.probe = s->tune.probe;
-            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->cached_rows, s->tune.blocks, s->tune.warps_per_block,
-                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows);
+            const cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
+                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window);
             // Each CTA trains its own replica of the hot rows between flushes; flushing
             // delta / n_CTA averages the replicas (local SGD + model averaging, as across
             // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every
             // CTA pushes the same top-of-tree correction, overshooting by ~n_CTA.
             h.hot_flush_scale = s->tune.hot_flush_scale > 0.0f ? s->tune.hot_flush_scale : 1.0f / static_cast<float>(g.blocks);
+            // Default per-row scale: 1 / E[#CTAs contributing to the row per flush period].
+            // A row on the paths of a share q of the centers is touched by a CTA within F
+            // merged centers with probability 1 - (1 - q)^F; averaging over that many
+            // replicas keeps the hot rows stable while deep cached rows still sum.
+            h.row_scale = nullptr;
+            if (s->tune.hot_flush_scale <= 0.0f && !s->row_share.empty() && g.cache_rows > 0) {
+                if (s->scale_blocks != g.blocks || s->scale_flush != h.flush_centers || s->scale_rows != g.cache_rows) {
+                    std::vector<float> sc(static_cast<size_t>(g.cache_rows));
+                    for (int32_t r = 0; r < g.cache_rows; ++r) {
+                        const double q = r < static_cast<int32_t>(s->row_share.size()) ? s->row_share[static_cast<size_t>(r)] : 0.0;
+                        const double p = 1.0 - std::pow(1.0 - std::min(q, 1.0), static_cast<double>(h.flush_centers));
+                        sc[static_cast<size_t>(r)] = static_cast<float>(1.0 / std::max(1.0, p * g.blocks));
+                    }
+                    s->row_scale.upload(sc.data(), sc.size(), s->stream);
+                    s->scale_blocks = g.blocks;
+                    s->scale_flush = h.flush_centers;
+                    s->scale_rows = g.cache_rows;
+                }
+                h.row_scale = s->row_scale.p;
+            }
             CG_CUDA(cudaEventRecord(s->ev[2], s->stream));
             cgk::launch_hogwild(h, g, s->stream);
             CG_CUDA(cudaGetLastError());

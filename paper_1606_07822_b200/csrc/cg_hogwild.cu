@@ -133,9 +133,14 @@ __global__ void __launch_bounds__(kSubThreads) sub_scatter_kernel(SubArgs a) {
 constexpr int kCodeSlots = 80;  // per-warp path codes: L <= 64 plus group padding
 
 // Worker warps train centers; warp `workers` (the last one) is the cache flusher.
-template <int DCH, int HMAX, int G, int WORKERS>
+//
+// Per center the warp runs "row-major": every path row is loaded once, trained against
+// all of the center's contexts in order (the row's own update sequence is exactly the
+// reference's), and written back with a single delta. G rows are processed together
+// (their dot products reduce in one transpose-reduce); the contexts' rows and their
+// hidden-layer accumulators h live in a per-warp shared-memory buffer.
+template <int DCH, int G, int WORKERS>
 __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
-    constexpr int LGH = Log2<HMAX>::v;
     constexpr int LGG = Log2<G>::v;
     extern __shared__ float4 hsm[];
     float* sig = reinterpret_cast<float*>(hsm);                      // 1024 floats
@@ -144,6 +149,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
     const int K = a.cache_rows;
     const int d4 = a.d4;
     int* locks = reinterpret_cast<int*>(dblk + K * d4);
+    float4* ctx_all = reinterpret_cast<float4*>(locks + ((K + 3) & ~3));  // WORKERS * 2 * NB * d4
+    const int NB = a.ctx_batch;
     __shared__ int s_done;
     __shared__ unsigned s_merged;
 
@@ -186,10 +193,11 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
                     __threadfence_block();
                     __syncwarp();
                     if (lane == 0) atomicExch(&locks[r], 0);
+                    const float sc = a.row_scale ? a.row_scale[r] : a.hot_flush_scale;
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
-                        if (q < d4 && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(a.hot_flush_scale, d[k]));
+                        if (q < d4 && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
                     }
                 }
                 __threadfence();  // publish the flush; also drops this SM's stale L1 lines of hot rows
@@ -202,6 +210,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 
     // ---- workers
     int* codes = codes_all + warp * kCodeSlots;
+    float4* V = ctx_all + static_cast<size_t>(warp) * 2 * NB * d4;  // context rows
+    float4* Hs = V + NB * d4;                                        // their h accumulators
     const int dummy_code = a.dummy_row << 1;
     const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
     const int cpw = a.centers_per_warp;
@@ -222,145 +232,142 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
                                                       static_cast<uint64_t>(a.window));
             const int64_t lo = max(s_lo, ci - b), hi = min(s_hi - 1, ci + b);
             ++n_centers;
-            if (hi == lo) continue;
+            const int n = static_cast<int>(hi - lo);  // contexts (the center itself excluded)
+            if (n == 0) continue;
             const int p0 = a.path_off[c];
             const int L = a.path_off[c + 1] - p0;
             __syncwarp();
             for (int j = lane; j < kCodeSlots; j += 32) codes[j] = j < L ? a.path_code[p0 + j] : dummy_code;
-            __syncwarp();
-            const unsigned hm = __ballot_sync(kFull, lane < L && (codes[lane] >> 1) < K);
-            const int H = hm == kFull ? 32 : __ffs(~hm) - 1;
-            const int Hp = min(H, HMAX);
+            bool touched_cache = false;
 
-            // private copy of the cached prefix: U = working rows, Q = this center's delta
-            float4 U[HMAX][DCH], Q[HMAX][DCH];
-#pragma unroll
-            for (int j = 0; j < HMAX; ++j) {
-                const int row = codes[j] >> 1;
-#pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    const int q = lane + 32 * k;
-                    float4 u = f4(0.f);
-                    if (j < Hp && q < d4) u = add4(ld_ca4(a.syn1 + 4 * (row * d4 + q)), dblk[row * d4 + q]);
-                    U[j][k] = u;
-                    Q[j][k] = f4(0.f);
-                }
-            }
-
-            for (int64_t xi = lo; xi <= hi; ++xi) {
-                if (xi == ci) continue;
-                const int xo = a.kept[xi] * d4;
-                float4 v[DCH], h[DCH];
-#pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    const int q = lane + 32 * k;
-                    v[k] = q < d4 ? ld_cg4(a.syn0 + 4 * (xo + q)) : f4(0.f);
-                    h[k] = f4(0.f);
-                }
-                // -- phase A: the cached prefix, on the private copy
-                if (Hp > 0) {
-                    float p[HMAX];
-#pragma unroll
-                    for (int j = 0; j < HMAX; ++j) {
-                        float acc = 0.f;
-#pragma unroll
-                        for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[j][k], acc);
-                        p[j] = acc;
-                    }
-                    const float tot = transpose_reduce<HMAX>(p, lane);
-                    const int jl = lane >> (5 - LGH);
-                    const float f = table_sigmoid(sig, tot, a.sig_scale);
-                    const float gl = (1.0f - static_cast<float>(codes[jl] & 1) - f) * alpha;
-#pragma unroll
-                    for (int j = 0; j < HMAX; ++j) {
-                        const float g = __shfl_sync(kFull, gl, j << (5 - LGH));
-                        if (j < Hp) {
-#pragma unroll
-                            for (int k = 0; k < DCH; ++k) {
-                                h[k] = axpy4(g, U[j][k], h[k]);
-                                U[j][k] = axpy4(g, v[k], U[j][k]);
-                                Q[j][k] = axpy4(g, v[k], Q[j][k]);
-                            }
-                        }
-                    }
-                }
-                // -- phase B: the rest of the path, G steps at a time (padded with a zero row)
-                for (int j0 = Hp; j0 < L; j0 += G) {
-                    float4 R[G][DCH];
-                    int ro[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        ro[g] = (codes[j0 + g] >> 1) * d4;
-#pragma unroll
-                        for (int k = 0; k < DCH; ++k) {
-                            const int q = lane + 32 * k;
-                            R[g][k] = q < d4 ? ld_cg4(a.syn1 + 4 * (ro[g] + q)) : f4(0.f);
-                        }
-                    }
-                    float p[G];
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        float acc = 0.f;
-#pragma unroll
-                        for (int k = 0; k < DCH; ++k) acc = dot4(v[k], R[g][k], acc);
-                        p[g] = acc;
-                    }
-                    const float tot = transpose_reduce<G>(p, lane);
-                    const int jl = j0 + (lane >> (5 - LGG));
-                    const float f = table_sigmoid(sig, tot, a.sig_scale);
-                    const float gl = jl < L ? (1.0f - static_cast<float>(codes[jl] & 1) - f) * alpha : 0.f;
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float gg = __shfl_sync(kFull, gl, g << (5 - LGG));
-                        const bool live = j0 + g < L;
-#pragma unroll
-                        for (int k = 0; k < DCH; ++k) {
-                            const int q = lane + 32 * k;
-                            h[k] = axpy4(gg, R[g][k], h[k]);
-                            if (live && q < d4) {
-                                if (a.probe & 1) {
-                                } else if (a.cold_store)
-                                    st_cg4(a.syn1 + 4 * (ro[g] + q), axpy4(gg, v[k], R[g][k]));
-                                else
-                                    red_add4(a.syn1 + 4 * (ro[g] + q), scale4(gg, v[k]));
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    const int q = lane + 32 * k;
-                    if (q < d4 && !(a.probe & 2)) {
-                        if (a.cold_store)
-                            st_cg4(a.syn0 + 4 * (xo + q), add4(v[k], h[k]));
-                        else
-                            red_add4(a.syn0 + 4 * (xo + q), h[k]);
-                    }
-                }
-                ++n_pairs;
-                n_steps += static_cast<unsigned long long>(L);
-            }
-            // merge the center's delta into the block cache (row locks) and count it
-#pragma unroll
-            for (int j = 0; j < HMAX; ++j) {
-                if (j < Hp && !(a.probe & 4)) {
-                    const int row = codes[j] >> 1;
-                    if (lane == 0)
-                        while (atomicCAS(&locks[row], 0, 1) != 0) {
-                        }
-                    __syncwarp();
-                    __threadfence_block();
+            for (int q0 = 0; q0 < n; q0 += NB) {
+                const int nb = min(NB, n - q0);
+                // stage this batch of context rows; h accumulators start at 0
+                for (int i = 0; i < nb; ++i) {
+                    int64_t pos = lo + q0 + i;
+                    pos += pos >= ci;  // skip the center's own position
+                    const int xo = a.kept[pos] * d4;
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
-                        if (q < d4) dblk[row * d4 + q] = add4(dblk[row * d4 + q], Q[j][k]);
+                        if (q < d4) {
+                            V[i * d4 + q] = ld_cg4(a.syn0 + 4 * (xo + q));
+                            Hs[i * d4 + q] = f4(0.f);
+                        }
                     }
-                    __threadfence_block();
-                    __syncwarp();
-                    if (lane == 0) atomicExch(&locks[row], 0);
                 }
+                __syncwarp();
+                for (int j0 = 0; j0 < L; j0 += G) {
+                    float4 U[G][DCH], S[G][DCH];
+                    int row[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        row[g] = codes[j0 + g] >> 1;
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            float4 u = f4(0.f);
+                            if (q < d4) {
+                                const int e = row[g] * d4 + q;
+                                u = row[g] < K ? add4(ld_ca4(a.syn1 + 4 * e), dblk[e]) : ld_cg4(a.syn1 + 4 * e);
+                            }
+                            U[g][k] = u;
+                            S[g][k] = u;
+                        }
+                    }
+                    const int jl = j0 + (lane >> (5 - LGG));
+                    const float turn = static_cast<float>(codes[jl] & 1);
+                    const bool jl_live = jl < L;
+                    for (int i = 0; i < nb; ++i) {
+                        float4 v[DCH];
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
+                        }
+                        float p[G];
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            float acc = 0.f;
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
+                            p[g] = acc;
+                        }
+                        const float tot = transpose_reduce<G>(p, lane);
+                        const float f = table_sigmoid(sig, tot, a.sig_scale);
+                        const float gl = jl_live ? (1.0f - turn - f) * alpha : 0.f;
+                        float4 hacc[DCH];
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) hacc[k] = f4(0.f);
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            const float gg = __shfl_sync(kFull, gl, g << (5 - LGG));
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                hacc[k] = axpy4(gg, U[g][k], hacc[k]);
+                                U[g][k] = axpy4(gg, v[k], U[g][k]);
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            if (q < d4) Hs[i * d4 + q] = add4(Hs[i * d4 + q], hacc[k]);
+                        }
+                    }
+                    // write back each row's delta once: block cache (locked) or HBM (red)
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        if (j0 + g >= L) continue;
+                        if (row[g] < K) {
+                            touched_cache = true;
+                            if (lane == 0)
+                                while (atomicCAS(&locks[row[g]], 0, 1) != 0) {
+                                }
+                            __syncwarp();
+                            __threadfence_block();
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (q < d4) {
+                                    const int e = row[g] * d4 + q;
+                                    dblk[e] = add4(dblk[e], make_float4(U[g][k].x - S[g][k].x, U[g][k].y - S[g][k].y,
+                                                                        U[g][k].z - S[g][k].z, U[g][k].w - S[g][k].w));
+                                }
+                            }
+                            __threadfence_block();
+                            __syncwarp();
+                            if (lane == 0) atomicExch(&locks[row[g]], 0);
+                        } else if (!(a.probe & 1)) {
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (q < d4)
+                                    red_add4(a.syn1 + 4 * (row[g] * d4 + q),
+                                             make_float4(U[g][k].x - S[g][k].x, U[g][k].y - S[g][k].y,
+                                                         U[g][k].z - S[g][k].z, U[g][k].w - S[g][k].w));
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                // the contexts' rows move once, by their accumulated h (trainer.hpp:173)
+                if (!(a.probe & 2)) {
+                    for (int i = 0; i < nb; ++i) {
+                        int64_t pos = lo + q0 + i;
+                        pos += pos >= ci;
+                        const int xo = a.kept[pos] * d4;
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            if (q < d4) red_add4(a.syn0 + 4 * (xo + q), Hs[i * d4 + q]);
+                        }
+                    }
+                }
+                __syncwarp();
             }
-            if (lane == 0 && Hp > 0) atomicAdd(&s_merged, 1u);
+            n_pairs += static_cast<unsigned long long>(n);
+            n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
+            if (lane == 0 && touched_cache) atomicAdd(&s_merged, 1u);
         }
     }
     if (lane == 0) {  // counts are warp-uniform
@@ -371,31 +378,32 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
     }
 }
 
-template <int DCH, int HMAX, int G, int WORKERS>
+template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = hog_kernel<DCH, HMAX, G, WORKERS>;
+    auto k = hog_kernel<DCH, G, WORKERS>;
     if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
     b.centers_per_warp = g.cpw;
+    b.ctx_batch = g.ctx_batch;
     k<<<g.blocks, (g.warps + 1) * 32, g.smem, s>>>(b);
 }
 
-// Per-variant shape: float4 chunks per lane (DCH), private cached prefix (HMAX),
-// cold-step group (G) and worker warps (register budget of the launch bounds).
+// Per-variant shape: float4 chunks per lane (DCH), rows trained together (G) and worker
+// warps (the register budget of the launch bounds).
 template <int DCH>
 struct Variant;
 template <>
 struct Variant<1> {
-    static constexpr int HMAX = 8, G = 8, WORKERS = 11;
+    static constexpr int G = 8, WORKERS = 15;
 };
 template <>
 struct Variant<2> {
-    static constexpr int HMAX = 4, G = 4, WORKERS = 11;
+    static constexpr int G = 4, WORKERS = 11;
 };
 template <>
 struct Variant<3> {
-    static constexpr int HMAX = 4, G = 4, WORKERS = 7;
+    static constexpr int G = 4, WORKERS = 7;
 };
 
 }  // namespace
@@ -415,16 +423,11 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
     if (launches) *launches = 3;
 }
 
-int hog_hmax(int d4) {
-    switch ((d4 + 31) / 32) {
-        case 1: return Variant<1>::HMAX;
-        case 2: return Variant<2>::HMAX;
-        default: return Variant<3>::HMAX;
-    }
-}
+// Every hot row can be cached (row-major processing has no private-prefix depth limit).
+int hog_hmax(int) { return 1 << 30; }
 
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override) {
+                     int rows_override, int window) {
     HogGeometry g{};
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -434,22 +437,26 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     g.warps = warps_override > 0 ? std::min(warps_override, workers) : workers;
     g.blocks = blocks_override > 0 ? blocks_override : sms;
     g.cpw = cpw_override > 0 ? cpw_override : 4;
+    // shared memory: sigmoid table | path codes | hot-row cache (+locks) | context buffers
     const size_t fixed = 4096 + static_cast<size_t>(workers) * kCodeSlots * 4;
-    const size_t budget = 110 * 1024;
     const size_t per_row = static_cast<size_t>(d4) * 16 + 4;
-    const int fit = static_cast<int>((budget - fixed) / per_row);
-    int rows = std::min(cache_rows_wanted, fit);
+    int rows = std::min(cache_rows_wanted, static_cast<int>((48 * 1024) / per_row));
     if (rows_override >= 0 && rows_override < rows) rows = rows_override;
     g.cache_rows = std::max(rows, 0);
-    g.smem = fixed + static_cast<size_t>(g.cache_rows) * per_row + 16;
+    const size_t cache_bytes = static_cast<size_t>(g.cache_rows) * d4 * 16 + static_cast<size_t>((g.cache_rows + 3) & ~3) * 4;
+    const size_t budget = 210 * 1024;
+    const size_t per_ctx = static_cast<size_t>(workers) * 2 * d4 * 16;
+    g.ctx_batch = static_cast<int>(std::min<size_t>(2 * static_cast<size_t>(window), (budget - fixed - cache_bytes) / per_ctx));
+    g.ctx_batch = std::max(g.ctx_batch, 1);
+    g.smem = fixed + cache_bytes + static_cast<size_t>(g.ctx_batch) * per_ctx;
     return g;
 }
 
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     switch (g.variant) {
-        case 1: launch_variant<1, Variant<1>::HMAX, Variant<1>::G, Variant<1>::WORKERS>(a, g, s); break;
-        case 2: launch_variant<2, Variant<2>::HMAX, Variant<2>::G, Variant<2>::WORKERS>(a, g, s); break;
-        default: launch_variant<3, Variant<3>::HMAX, Variant<3>::G, Variant<3>::WORKERS>(a, g, s); break;
+        case 1: launch_variant<1, Variant<1>::G, Variant<1>::WORKERS>(a, g, s); break;
+        case 2: launch_variant<2, Variant<2>::G, Variant<2>::WORKERS>(a, g, s); break;
+        default: launch_variant<3, Variant<3>::G, Variant<3>::WORKERS>(a, g, s); break;
     }
 }
 

@@ -109,9 +109,11 @@ struct HogArgs {
     int32_t cache_rows;        // K rows cached in shared memory (rows [0, K))
     int32_t centers_per_warp;
     int32_t cold_store;        // 1: plain stores for cold rows and syn0 (lossy Hogwild)
-    float hot_flush_scale;     // multiplier on block-cache deltas at flush
+    float hot_flush_scale;     // multiplier on block-cache deltas at flush (if row_scale == nullptr)
+    const float* row_scale;    // per cached row flush multiplier, or nullptr
     int32_t flush_centers;     // centers merged into a block cache between flushes
     int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
+    int32_t ctx_batch;         // context rows staged per warp (<= 2 * window)
     int32_t probe;             // experiments only: 1 skip cold-row updates, 2 skip syn0 updates, 4 skip cache merges
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
@@ -120,14 +122,15 @@ struct HogGeometry {
     int blocks;     // grid
     int cpw;        // centers per warp per tile
     int cache_rows;
+    int ctx_batch;  // contexts staged per warp
     int variant;    // DCH
     size_t smem;
 };
-// Private cached-prefix depth of the kernel variant for this row width.
+// Depth limit on cached hot rows for this row width (none for the row-major kernel).
 int hog_hmax(int d4);
 // Picks the kernel variant for d4 and the launch geometry for the device.
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override);
+                     int rows_override, int window);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 }  // namespace cgk

@@ -57,6 +57,8 @@ def main():
               flush=True)
 
     grids = {}
+    grids["kscale"] = [dict(k=0), dict(k=0, minrows=-1), dict(k=31), dict(k=64), dict(k=255), dict(k=1024),
+                       dict(k=31, scale=1 / 148), dict(k=255, scale=1 / 148)]
     grids["scales"] = [dict(k=0)] + [dict(k=k, scale=sc) for k in (31, 255) for sc in (1 / 148, 1 / 64, 1 / 32, 1 / 16, 1 / 8)]
     grids["probe"] = [dict(), dict(probe=1), dict(probe=2), dict(probe=3), dict(probe=4), dict(probe=7),
                       dict(k=0, probe=1), dict(cold=1)]
@@ -73,7 +75,7 @@ def main():
         cfg = api.TrainConfig(**dict(cfgd, cache_nodes=k), mode="hogwild")
         s = api.Session(vocab, tree, sel, cfg)
         s.tune(g.get("blocks", 0), g.get("warps", 0), g.get("cpw", 0), -1, g.get("cold", 0), g.get("scale", 0.0),
-               g.get("flush", 0), g.get("probe", 0))
+               g.get("flush", 0), g.get("minrows", 0), g.get("probe", 0))
         s.upload_ids(ids)
         ms = 0.0
         for it in range(a.iterations):
