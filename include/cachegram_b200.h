@@ -94,6 +94,9 @@ typedef struct cg_train_stats {
 /* ---- library --------------------------------------------------------------- */
 CG_API int cg_abi_version(void);
 CG_API const char* cg_last_error(void);
+/* Device buffers are pooled across calls (cg_train, sessions); this returns the cached,
+ * currently unused ones to the driver. */
+CG_API void cg_release_cached_memory(void);
 /* Number of visible CUDA devices (0 when none); never falls back. */
 CG_API int cg_device_count(void);
 

@@ -95,6 +95,7 @@ SIGNATURES = {
     "cg_abi_version": (C.c_int, []),
     "cg_last_error": (C.c_char_p, []),
     "cg_device_count": (C.c_int, []),
+    "cg_release_cached_memory": (None, []),
     "cg_keep_probability": (C.c_double, [C.c_int64, C.c_int64, C.c_double]),
     "cg_update_alpha": (C.c_float, [C.c_uint64, C.c_uint64, C.c_float]),
     "cg_sigmoid_table": (None, [P(C.c_float)]),
