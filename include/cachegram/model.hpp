@@ -11,9 +11,13 @@
 #include <cstdint>
 #include <span>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
+#include "cachegram/corpus.hpp"
+#include "cachegram/errors.hpp"
 #include "cachegram/rng.hpp"
+#include "cachegram_b200.h"
 
 namespace cachegram {
 
@@ -93,5 +97,101 @@ private:
 struct ExactSigmoid {
     float operator()(float x) const { return static_cast<float>(exact_sigmoid(static_cast<double>(x))); }
 };
+
+// ---------------------------------------------------------------------------------
+// Model files (model.hpp:107-276 of the reference): the input vectors plus the word
+// list, as text ("V D" header, "word v1 ... vD" rows, %.6f) or binary ("word " + raw
+// float32 + newline). Implemented in libcachegram_b200 (cg_modelio.cpp): the same bytes
+// and the same accepted inputs, with text formatting/parsing spread over host cores.
+// ---------------------------------------------------------------------------------
+namespace model_detail {
+[[noreturn]] inline void rethrow_io(int rc) {
+    const std::string msg = cg_last_error();
+    switch (rc) {
+        case CG_ERR_IO: throw IoError(msg);
+        case CG_ERR_PARSE: throw ParseError(msg);
+        case CG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+inline void check_io(int rc) {
+    if (rc != CG_OK) rethrow_io(rc);
+}
+inline std::string joined_words(const Vocabulary& vocab, std::int32_t n) {
+    std::string out;
+    for (std::int32_t w = 0; w < n; ++w) {
+        out += vocab.word(w);
+        out.push_back('\0');
+    }
+    return out;
+}
+inline void save(const Model& model, const Vocabulary& vocab, const std::string& path, std::int32_t format) {
+    const std::string words = joined_words(vocab, model.vocab_size());
+    check_io(cg_model_save(path.c_str(), format, words.data(), model.input_matrix().data(), model.vocab_size(),
+                           model.dim()));
+}
+}  // namespace model_detail
+
+inline void save_text(const Model& model, const Vocabulary& vocab, const std::string& path) {
+    model_detail::save(model, vocab, path, CG_FORMAT_TEXT);
+}
+
+inline void save_binary(const Model& model, const Vocabulary& vocab, const std::string& path) {
+    model_detail::save(model, vocab, path, CG_FORMAT_BINARY);
+}
+
+// What a model file stores: the word list in id order and the input vectors.
+struct LoadedEmbeddings {
+    std::int32_t dim = 0;
+    std::vector<std::string> words;
+    std::vector<float> vectors;  // words.size() x dim, row-major
+
+    std::int32_t size() const { return static_cast<std::int32_t>(words.size()); }
+    const float* vector(std::int32_t w) const {
+        return vectors.data() + static_cast<std::size_t>(w) * static_cast<std::size_t>(dim);
+    }
+};
+
+inline LoadedEmbeddings to_embeddings(const Model& model, const Vocabulary& vocab) {
+    LoadedEmbeddings out;
+    out.dim = model.dim();
+    out.words.reserve(static_cast<std::size_t>(vocab.size()));
+    for (std::int32_t w = 0; w < vocab.size(); ++w) out.words.push_back(vocab.word(w));
+    out.vectors.assign(model.input_matrix().begin(), model.input_matrix().end());
+    return out;
+}
+
+namespace model_detail {
+inline LoadedEmbeddings load(const std::string& path, std::int32_t format) {
+    cg_embeddings_file* f = nullptr;
+    check_io(cg_model_load(path.c_str(), format, &f));
+    struct Closer {
+        cg_embeddings_file* f;
+        ~Closer() { cg_model_file_close(f); }
+    } closer{f};
+    std::int32_t v = 0, d = 0;
+    std::int64_t word_bytes = 0;
+    check_io(cg_model_file_info(f, &v, &d, &word_bytes));
+    std::string words(static_cast<std::size_t>(word_bytes), '\0');
+    LoadedEmbeddings out;
+    out.dim = d;
+    out.vectors.resize(static_cast<std::size_t>(v) * static_cast<std::size_t>(d));
+    check_io(cg_model_file_export(f, words.data(), out.vectors.data()));
+    out.words.reserve(static_cast<std::size_t>(v));
+    for (std::size_t p = 0; p < words.size();) {
+        const std::size_t e = words.find('\0', p);
+        out.words.emplace_back(words, p, e - p);
+        p = e + 1;
+    }
+    return out;
+}
+}  // namespace model_detail
+
+inline LoadedEmbeddings load_embeddings_binary(const std::string& path) {
+    return model_detail::load(path, CG_FORMAT_BINARY);
+}
+inline LoadedEmbeddings load_embeddings_text(const std::string& path) { return model_detail::load(path, CG_FORMAT_TEXT); }
+// Either format: a binary file is recognised by a non-printable byte after the header.
+inline LoadedEmbeddings load_embeddings(const std::string& path) { return model_detail::load(path, CG_FORMAT_AUTO); }
 
 }  // namespace cachegram

@@ -107,6 +107,7 @@ namespace trainer_detail {
     switch (rc) {
         case CG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
         case CG_ERR_IO: throw IoError(msg);
+        case CG_ERR_PARSE: throw ParseError(msg);
         case CG_ERR_NO_TRAINABLE_WORDS: throw NoTrainableWords();
         default: throw std::runtime_error(msg);
     }

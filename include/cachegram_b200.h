@@ -10,7 +10,7 @@
  *
  * Status codes map onto the reference's exceptions (trainer.hpp:37-47, 256-260;
  * corpus.hpp:194,232; errors.hpp:12-24): CG_ERR_INVALID_ARGUMENT -> std::invalid_argument,
- * CG_ERR_IO -> IoError, CG_ERR_NO_TRAINABLE_WORDS -> NoTrainableWords, the rest ->
+ * CG_ERR_IO -> IoError, CG_ERR_PARSE -> ParseError, CG_ERR_NO_TRAINABLE_WORDS -> NoTrainableWords, the rest ->
  * std::runtime_error. The message is in cg_last_error() (thread-local).
  *
  * Everything that computes on the training path runs on the GPU; there is no CPU
@@ -42,7 +42,8 @@ enum cg_status {
     CG_ERR_CUDA = 3,
     CG_ERR_NCCL = 4,
     CG_ERR_NO_TRAINABLE_WORDS = 5,
-    CG_ERR_INTERNAL = 6
+    CG_ERR_INTERNAL = 6,
+    CG_ERR_PARSE = 7 /* a model or question file violates its format -> ParseError */
 };
 
 /* Training modes. DETERMINISTIC replays the reference's single-worker stream
@@ -216,8 +217,49 @@ typedef struct cg_tuning {
                                  even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
                                  context-row updates, bit 2 skip cache merges */
+    int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
+
+/* ---- evaluation (eval.hpp:88-238) ---------------------------
+ * A device-resident table of unit-normalised rows, built exactly like AnalogySolver
+ * (eval.hpp:91-103): row / sqrtf(dot(row, row)), zeros when the norm is not > 0.
+ * Scores are the reference's sequential fp32 dot, so answers match it bit for bit. */
+typedef struct cg_embeddings cg_embeddings;
+/* rows = AnalogySolver::vocab_size() = min(V, restrict_top) (first rows of `vectors`).
+ * device < 0 selects the calling thread's current CUDA device. */
+CG_API int cg_embeddings_create(const float* vectors, int32_t rows, int32_t dim, int32_t device, cg_embeddings** out);
+/* Same from device memory (e.g. a session's syn0, row_stride floats apart); no host copy. */
+CG_API int cg_embeddings_create_device(const float* device_vectors, int32_t rows, int32_t dim, int32_t row_stride,
+                                       int32_t device, cg_embeddings** out);
+CG_API void cg_embeddings_destroy(cg_embeddings* e);
+CG_API int32_t cg_embeddings_rows(const cg_embeddings* e);
+/* The normalised rows (rows x dim, host). */
+CG_API int cg_embeddings_normalized(const cg_embeddings* e, float* out);
+/* AnalogySolver::answer (eval.hpp:117-136) for n questions: abc = [a0,b0,c0, a1,b1,c1, ...]
+ * (ids < rows), best[i] = argmax_w cos(v(b)-v(a)+v(c), v(w)) over w not in {a,b,c}, ties to
+ * the lower id, -1 when no candidate is left. */
+CG_API int cg_analogy_answer(cg_embeddings* e, const int32_t* abc, int64_t n, int32_t* best);
+/* Cosine top-k neighbours (k <= 32) of the query rows, excluding the query's own row,
+ * ranked by the same exact scores with ties to the lower id: the recall@k metric of
+ * SURVEY 8(d). ids[i*k + r] = -1 (score NaN) when fewer than k candidates exist. */
+CG_API int cg_nearest(cg_embeddings* e, const int32_t* queries, int64_t n, int32_t k, int32_t* ids, float* scores);
+
+/* ---- model files (model.hpp:107-276) ---------------------------------------------
+ * Text:   "V D\n" then "word v1 ... vD\n" per word, values as " %.6f".
+ * Binary: "V D\n" then "word " + D little-endian float32 + "\n" per word.
+ * words_nul: the V words, each NUL-terminated, in id order. Text formatting runs on
+ * all host cores; the bytes equal the reference's single-threaded fprintf output. */
+enum cg_model_format { CG_FORMAT_TEXT = 0, CG_FORMAT_BINARY = 1, CG_FORMAT_AUTO = 2 };
+CG_API int cg_model_save(const char* path, int32_t format, const char* words_nul, const float* syn0, int32_t vocab_size,
+                         int32_t dim);
+/* Two-call load: open parses the file (format AUTO detects it as load_embeddings does),
+ * info reports the sizes, export copies words (NUL-separated) and vectors out. */
+typedef struct cg_embeddings_file cg_embeddings_file;
+CG_API int cg_model_load(const char* path, int32_t format, cg_embeddings_file** out);
+CG_API int cg_model_file_info(const cg_embeddings_file* f, int32_t* vocab_size, int32_t* dim, int64_t* word_bytes);
+CG_API int cg_model_file_export(const cg_embeddings_file* f, char* words_nul, float* vectors);
+CG_API void cg_model_file_close(cg_embeddings_file* f);
 
 #ifdef __cplusplus
 }

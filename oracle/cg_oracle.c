@@ -424,3 +424,81 @@ int64_t orc_sample_pairs(const int32_t* ids, int64_t n_ids, const float* keep, i
     }
     return got;
 }
+
+
+/* ---------------------------------------------------------------- evaluation */
+/* vec_ops.hpp:14-18: sum from +0, ascending i, separately rounded mul and add. */
+static float orc_dot(const float* a, const float* b, int32_t n) {
+    float s = 0.0f;
+    for (int32_t i = 0; i < n; ++i) {
+        const float p = a[i] * b[i];
+        s = s + p;
+    }
+    return s;
+}
+
+/* eval.hpp:91-103 */
+void orc_normalize(const float* src, int64_t rows, int32_t dim, float* out) {
+    for (int64_t r = 0; r < rows; ++r) {
+        const float* x = src + r * dim;
+        float* y = out + r * dim;
+        const float norm = sqrtf(orc_dot(x, x, dim));
+        for (int32_t d = 0; d < dim; ++d) y[d] = norm > 0.0f ? x[d] / norm : 0.0f;
+    }
+}
+
+/* eval.hpp:117-136: target = (vb - va) + vc; the first candidate seeds `best`, later
+ * ones replace it only when strictly greater. */
+void orc_analogy(const float* norm, int64_t rows, int32_t dim, const int32_t* abc, int64_t n, int32_t* out) {
+    float* t = (float*)malloc(sizeof(float) * (size_t)(dim > 0 ? dim : 1));
+    for (int64_t q = 0; q < n; ++q) {
+        const int32_t a = abc[3 * q], b = abc[3 * q + 1], c = abc[3 * q + 2];
+        for (int32_t d = 0; d < dim; ++d) {
+            const float diff = norm[(int64_t)b * dim + d] - norm[(int64_t)a * dim + d];
+            t[d] = diff + norm[(int64_t)c * dim + d];
+        }
+        int32_t best = -1;
+        float best_score = 0.0f;
+        for (int64_t w = 0; w < rows; ++w) {
+            if (w == a || w == b || w == c) continue;
+            const float s = orc_dot(t, norm + w * dim, dim);
+            if (best < 0 || s > best_score) {
+                best = (int32_t)w;
+                best_score = s;
+            }
+        }
+        out[q] = best;
+    }
+    free(t);
+}
+
+void orc_topk(const float* norm, int64_t rows, int32_t dim, const int32_t* queries, int64_t n, int32_t k,
+              int32_t* ids, float* scores) {
+    for (int64_t q = 0; q < n; ++q) {
+        int32_t* qi = ids + q * k;
+        float* qs = scores + q * k;
+        int32_t filled = 0;
+        for (int32_t r = 0; r < k; ++r) {
+            qi[r] = -1;
+            qs[r] = NAN;
+        }
+        const float* x = norm + (int64_t)queries[q] * dim;
+        for (int64_t w = 0; w < rows; ++w) {
+            if (w == queries[q]) continue;
+            const float s = orc_dot(x, norm + w * dim, dim);
+            if (isnan(s)) continue;
+            /* insertion: strictly greater moves ahead, so equal scores keep the lower id first */
+            int32_t pos = filled;
+            while (pos > 0 && s > qs[pos - 1]) --pos;
+            if (pos >= k) continue;
+            const int32_t last = filled < k ? filled : k - 1;
+            for (int32_t r = last; r > pos; --r) {
+                qi[r] = qi[r - 1];
+                qs[r] = qs[r - 1];
+            }
+            qi[pos] = (int32_t)w;
+            qs[pos] = s;
+            if (filled < k) ++filled;
+        }
+    }
+}

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "cachegram/corpus.hpp"
+#include "cachegram/eval.hpp"
 #include "cachegram/huffman.hpp"
 #include "cachegram/model.hpp"
 #include "cachegram/rng.hpp"
@@ -226,6 +227,77 @@ int64_t ref_train_center(const int64_t* counts, int32_t v, int32_t dim, float* s
     std::memcpy(syn0, model.input_matrix().data(), model.input_matrix().size() * sizeof(float));
     std::memcpy(syn1, model.weight_matrix().data(), model.weight_matrix().size() * sizeof(float));
     return evals;
+}
+
+// ---- evaluation and model files (eval.hpp, model.hpp:107-276) ---------------
+namespace {
+LoadedEmbeddings embeddings_of(const float* vectors, int32_t rows, int32_t dim) {
+    LoadedEmbeddings e;
+    e.dim = dim;
+    for (int32_t w = 0; w < rows; ++w) e.words.push_back("w" + std::to_string(w));
+    e.vectors.assign(vectors, vectors + static_cast<size_t>(rows) * dim);
+    return e;
+}
+}  // namespace
+
+// AnalogySolver(embeddings, restrict_top).answer(a, b, c) for n questions.
+int ref_analogy(const float* vectors, int32_t rows, int32_t dim, int32_t restrict_top, const int32_t* abc, int64_t n,
+                int32_t* out) {
+    try {
+        const AnalogySolver solver(embeddings_of(vectors, rows, dim), restrict_top);
+        for (int64_t q = 0; q < n; ++q) out[q] = solver.answer(abc[3 * q], abc[3 * q + 1], abc[3 * q + 2]);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// save_text (binary == 0) or save_binary of a model whose words are NUL-separated.
+int ref_model_save(const char* path, int32_t binary, const char* words_nul, const float* syn0, int32_t v, int32_t d) {
+    try {
+        std::vector<VocabEntry> entries;
+        const char* p = words_nul;
+        for (int32_t i = 0; i < v; ++i) {
+            entries.push_back({std::string(p), 1});
+            p += std::strlen(p) + 1;
+        }
+        const Vocabulary vocab(std::move(entries), v);
+        Model m(v, d);
+        std::memcpy(m.input_matrix().data(), syn0, sizeof(float) * static_cast<size_t>(v) * d);
+        if (binary)
+            save_binary(m, vocab, path);
+        else
+            save_text(m, vocab, path);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// load_embeddings (format 2), load_embeddings_text (0) or load_embeddings_binary (1).
+// Returns 0 and fills rows/dim/vectors (capacity floats) or -1 IoError / -2 ParseError.
+int ref_model_load(const char* path, int32_t format, int32_t* rows, int32_t* dim, float* vectors, int64_t capacity) {
+    try {
+        const LoadedEmbeddings e = format == 0   ? load_embeddings_text(path)
+                                   : format == 1 ? load_embeddings_binary(path)
+                                                 : load_embeddings(path);
+        *rows = e.size();
+        *dim = e.dim;
+        if (vectors && static_cast<int64_t>(e.vectors.size()) <= capacity)
+            std::memcpy(vectors, e.vectors.data(), e.vectors.size() * sizeof(float));
+        return 0;
+    } catch (const IoError& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const ParseError& e) {
+        g_err = e.what();
+        return -2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -3;
+    }
 }
 
 #pragma GCC visibility pop

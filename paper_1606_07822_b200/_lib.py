@@ -22,6 +22,11 @@ CG_ERR_CUDA = 3
 CG_ERR_NCCL = 4
 CG_ERR_NO_TRAINABLE_WORDS = 5
 CG_ERR_INTERNAL = 6
+CG_ERR_PARSE = 7
+
+CG_FORMAT_TEXT = 0
+CG_FORMAT_BINARY = 1
+CG_FORMAT_AUTO = 2
 
 CG_MODE_HOGWILD = 0
 CG_MODE_DETERMINISTIC = 1
@@ -84,7 +89,8 @@ class CgEpochStats(C.Structure):
 class CgTuning(C.Structure):
     _fields_ = [("blocks", C.c_int32), ("warps_per_block", C.c_int32), ("centers_per_warp", C.c_int32),
                 ("smem_cache_rows", C.c_int32), ("cold_update", C.c_int32), ("hot_flush_scale", C.c_float),
-                ("flush_centers", C.c_int32), ("min_cache_rows", C.c_int32), ("probe", C.c_int32)]
+                ("flush_centers", C.c_int32), ("min_cache_rows", C.c_int32), ("probe", C.c_int32),
+                ("kernel", C.c_int32)]
 
 
 P = C.POINTER
@@ -134,6 +140,18 @@ SIGNATURES = {
     "cg_session_download": (C.c_int, [vp, P(C.c_float), P(C.c_float)]),
     "cg_session_model_buffer": (C.c_int, [vp, P(vp), P(C.c_size_t), P(C.c_int32)]),
     "cg_session_tune": (C.c_int, [vp, P(CgTuning)]),
+    "cg_embeddings_create": (C.c_int, [P(C.c_float), C.c_int32, C.c_int32, C.c_int32, P(vp)]),
+    "cg_embeddings_create_device": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(vp)]),
+    "cg_embeddings_destroy": (None, [vp]),
+    "cg_embeddings_rows": (C.c_int32, [vp]),
+    "cg_embeddings_normalized": (C.c_int, [vp, P(C.c_float)]),
+    "cg_analogy_answer": (C.c_int, [vp, P(C.c_int32), C.c_int64, P(C.c_int32)]),
+    "cg_nearest": (C.c_int, [vp, P(C.c_int32), C.c_int64, C.c_int32, P(C.c_int32), P(C.c_float)]),
+    "cg_model_save": (C.c_int, [C.c_char_p, C.c_int32, C.c_char_p, P(C.c_float), C.c_int32, C.c_int32]),
+    "cg_model_load": (C.c_int, [C.c_char_p, C.c_int32, P(vp)]),
+    "cg_model_file_info": (C.c_int, [vp, P(C.c_int32), P(C.c_int32), P(C.c_int64)]),
+    "cg_model_file_export": (C.c_int, [vp, C.c_char_p, P(C.c_float)]),
+    "cg_model_file_close": (None, [vp]),
 }
 
 _lib = None
@@ -161,6 +179,10 @@ def exported_symbols() -> list[str]:
     return list(SIGNATURES)
 
 
+class ParseError(RuntimeError):
+    """A model or question file violates its format (the reference's ParseError)."""
+
+
 class CgError(RuntimeError):
     def __init__(self, code: int, message: str):
         super().__init__(message)
@@ -174,6 +196,8 @@ def check(rc: int) -> None:
             raise ValueError(msg)
         if rc == CG_ERR_IO:
             raise OSError(msg)
+        if rc == CG_ERR_PARSE:
+            raise ParseError(msg)
         raise CgError(rc, msg)
 
 

@@ -456,9 +456,9 @@ class Session:
 
     def tune(self, blocks: int = 0, warps: int = 0, centers_per_warp: int = 0, cache_rows: int = -1,
              cold_update: int = 0, hot_flush_scale: float = 0.0, flush_centers: int = 0, min_cache_rows: int = 0,
-             probe: int = 0) -> None:
+             probe: int = 0, kernel: int = 0) -> None:
         t = _lib.CgTuning(blocks, warps, centers_per_warp, cache_rows, cold_update, hot_flush_scale, flush_centers,
-                          min_cache_rows, probe)
+                          min_cache_rows, probe, kernel)
         check(load().cg_session_tune(self._h, C.byref(t)))
 
     def train_range(self, epoch: int, begin: int, end: int, progress_base: int = 0,
@@ -495,3 +495,224 @@ class Session:
             __cuda_array_interface__ = {"shape": (n // 4,), "typestr": "<f4", "data": (p, False), "version": 3}
 
         return torch.as_tensor(_Cai(), device="cuda")
+
+
+# --------------------------------------------------------------------------- model files
+@dataclass
+class LoadedEmbeddings:
+    """model.hpp:147-157: the word list in id order and the input vectors (V x D)."""
+    dim: int
+    words: list
+    vectors: np.ndarray
+
+    def size(self) -> int:
+        return len(self.words)
+
+    def vector(self, w: int) -> np.ndarray:
+        return self.vectors[w]
+
+
+def _words_nul(words) -> bytes:
+    return b"".join(w.encode() + b"\0" for w in words)
+
+
+def _save(model: Model, vocab: Vocabulary, path: str, fmt: int) -> None:
+    syn0 = np.ascontiguousarray(model.syn0, dtype=np.float32)
+    words = _words_nul(vocab.word(w) for w in range(model.vocab_size()))
+    check(load().cg_model_save(str(path).encode(), fmt, words, ptr(syn0, C.c_float), model.vocab_size(), model.dim()))
+
+
+def save_text(model: Model, vocab: Vocabulary, path: str) -> None:
+    """model.hpp:119-130 ("V D" header, "word v1 ... vD" rows with %.6f)."""
+    _save(model, vocab, path, _lib.CG_FORMAT_TEXT)
+
+
+def save_binary(model: Model, vocab: Vocabulary, path: str) -> None:
+    """model.hpp:132-144 ("word " + D little-endian float32 + newline per row)."""
+    _save(model, vocab, path, _lib.CG_FORMAT_BINARY)
+
+
+def to_embeddings(model: Model, vocab: Vocabulary) -> LoadedEmbeddings:
+    """model.hpp:159-168."""
+    return LoadedEmbeddings(model.dim(), [vocab.word(w) for w in range(vocab.size())],
+                            np.array(model.syn0, dtype=np.float32, copy=True))
+
+
+def _load(path: str, fmt: int) -> LoadedEmbeddings:
+    lib = load()
+    h = C.c_void_p()
+    check(lib.cg_model_load(str(path).encode(), fmt, C.byref(h)))
+    try:
+        v, d, nb = C.c_int32(), C.c_int32(), C.c_int64()
+        check(lib.cg_model_file_info(h, C.byref(v), C.byref(d), C.byref(nb)))
+        buf = C.create_string_buffer(int(nb.value) + 1)
+        vec = np.empty((v.value, d.value), dtype=np.float32)
+        check(lib.cg_model_file_export(h, buf, ptr(vec, C.c_float)))
+        words = [w.decode("utf-8", "surrogateescape") for w in buf.raw[: nb.value].split(b"\0")[: v.value]]
+        return LoadedEmbeddings(d.value, words, vec)
+    finally:
+        lib.cg_model_file_close(h)
+
+
+def load_embeddings_binary(path: str) -> LoadedEmbeddings:
+    return _load(path, _lib.CG_FORMAT_BINARY)
+
+
+def load_embeddings_text(path: str) -> LoadedEmbeddings:
+    return _load(path, _lib.CG_FORMAT_TEXT)
+
+
+def load_embeddings(path: str) -> LoadedEmbeddings:
+    """Either format (model.hpp:249-274 auto-detection)."""
+    return _load(path, _lib.CG_FORMAT_AUTO)
+
+
+# --------------------------------------------------------------------------- evaluation
+class Embeddings:
+    """Device-resident unit-normalised rows (AnalogySolver's table, eval.hpp:91-103).
+    Built from host vectors, or zero-copy from a device pointer (e.g. a session's syn0)."""
+
+    def __init__(self, vectors: np.ndarray | None = None, *, rows: int | None = None, dim: int | None = None,
+                 device_ptr: int | None = None, row_stride: int | None = None, device: int = -1):
+        lib = load()
+        self._h = C.c_void_p()
+        if device_ptr is not None:
+            check(lib.cg_embeddings_create_device(C.c_void_p(device_ptr), int(rows), int(dim), int(row_stride or dim),
+                                                  int(device), C.byref(self._h)))
+            self.rows, self.dim = int(rows), int(dim)
+        else:
+            v = np.ascontiguousarray(vectors, dtype=np.float32)
+            r = v.shape[0] if rows is None else int(rows)
+            self.rows, self.dim = r, int(v.shape[1] if dim is None else dim)
+            check(lib.cg_embeddings_create(ptr(v, C.c_float), r, self.dim, int(device), C.byref(self._h)))
+
+    def normalized(self) -> np.ndarray:
+        out = np.empty((self.rows, self.dim), dtype=np.float32)
+        check(load().cg_embeddings_normalized(self._h, ptr(out, C.c_float)))
+        return out
+
+    def analogy(self, abc: np.ndarray) -> np.ndarray:
+        """abc: (n, 3) ids -> (n,) answers (eval.hpp:117-136)."""
+        q = np.ascontiguousarray(abc, dtype=np.int32).reshape(-1, 3)
+        out = np.full(q.shape[0], -1, dtype=np.int32)
+        check(load().cg_analogy_answer(self._h, ptr(q, C.c_int32), q.shape[0], ptr(out, C.c_int32)))
+        return out
+
+    def nearest(self, queries: np.ndarray, k: int = 10) -> tuple[np.ndarray, np.ndarray]:
+        """Exact cosine top-k (self excluded, ties to the lower id): ids (n, k), scores (n, k)."""
+        q = np.ascontiguousarray(queries, dtype=np.int32).reshape(-1)
+        ids = np.empty((q.size, k), dtype=np.int32)
+        sc = np.empty((q.size, k), dtype=np.float32)
+        check(load().cg_nearest(self._h, ptr(q, C.c_int32), q.size, int(k), ptr(ids, C.c_int32), ptr(sc, C.c_float)))
+        return ids, sc
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            load().cg_embeddings_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class AnalogyQuestion:
+    a: str
+    b: str
+    c: str
+    d: str
+    section: int = 0
+
+
+@dataclass
+class QuestionSet:
+    sections: list = field(default_factory=list)
+    questions: list = field(default_factory=list)
+
+
+def _tokens(line: str) -> list:
+    return [t for t in line.replace("\t", " ").replace("\r", " ").replace("\v", " ").replace("\f", " ").split(" ") if t]
+
+
+def load_questions(path: str) -> QuestionSet:
+    """eval.hpp:43-80: ": name" opens a section; other non-blank lines hold 4 words."""
+    try:
+        f = open(path, "rb")
+    except OSError as e:
+        raise OSError(f"cannot open question file: {path}") from e
+    qs = QuestionSet()
+    cur = -1
+    with f:
+        for no, raw in enumerate(f.read().decode("utf-8", "surrogateescape").split("\n"), start=1):
+            tok = _tokens(raw)
+            if not tok:
+                continue
+            if tok[0].startswith(":"):
+                parts = [t for t in [tok[0][1:], *tok[1:]] if t]
+                qs.sections.append(" ".join(parts) or "(unnamed)")
+                cur = len(qs.sections) - 1
+                continue
+            if len(tok) != 4:
+                raise _lib.ParseError(f"{path}:{no}: expected 4 words per question, got {len(tok)}")
+            if cur < 0:
+                qs.sections.append("(no section)")
+                cur = 0
+            low = [t.translate(str.maketrans("ABCDEFGHIJKLMNOPQRSTUVWXYZ", "abcdefghijklmnopqrstuvwxyz")) for t in tok]
+            qs.questions.append(AnalogyQuestion(*low, section=cur))
+    return qs
+
+
+class AnalogySolver:
+    """eval.hpp:85-150: 3CosAdd over the restrict_top most frequent words, on the GPU."""
+
+    def __init__(self, emb: LoadedEmbeddings, restrict_top: int):
+        self.size = min(emb.size(), restrict_top) if restrict_top > 0 else emb.size()
+        self.table = Embeddings(emb.vectors[: self.size], rows=self.size, dim=emb.dim)
+        self._index = {}
+        for w in range(self.size):
+            self._index.setdefault(emb.words[w], w)
+
+    def vocab_size(self) -> int:
+        return self.size
+
+    def id_of(self, word: str) -> int:
+        return self._index.get(word, -1)
+
+    def answer(self, a: int, b: int, c: int) -> int:
+        return int(self.table.analogy(np.array([[a, b, c]]))[0])
+
+
+@dataclass
+class SectionResult:
+    name: str
+    attempted: int = 0
+    skipped: int = 0
+    correct: int = 0
+
+    def accuracy(self):
+        return None if self.attempted == 0 else self.correct / self.attempted
+
+
+@dataclass
+class EvalReport:
+    sections: list = field(default_factory=list)
+    total: SectionResult = field(default_factory=lambda: SectionResult("TOTAL"))
+
+
+def evaluate(emb: LoadedEmbeddings, questions: QuestionSet, restrict_top: int, threads: int = 1) -> EvalReport:
+    """eval.hpp:165-225, every resolvable question answered in one device batch."""
+    solver = AnalogySolver(emb, restrict_top)
+    rep = EvalReport([SectionResult(n) for n in questions.sections])
+    abc, want, sec = [], [], []
+    for q in questions.questions:
+        ids = [solver.id_of(x) for x in (q.a, q.b, q.c, q.d)]
+        if min(ids) < 0:
+            rep.sections[q.section].skipped += 1
+            rep.total.skipped += 1
+            continue
+        abc.append(ids[:3])
+        want.append(ids[3])
+        sec.append(q.section)
+    got = solver.table.analogy(np.array(abc, dtype=np.int32).reshape(-1, 3)) if abc else np.empty(0, np.int32)
+    for g, w, s in zip(got, want, sec):
+        for r in (rep.sections[s], rep.total):
+            r.attempted += 1
+            r.correct += int(g == w)
+    return rep

@@ -11,8 +11,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libcachegram_b200.so"
-SOURCES = ["cg_capi.cu", "cg_det.cu", "cg_hogwild.cu"]
-HEADERS = ["cg_device.cuh", "cg_kernels.h"]
+SOURCES = ["cg_capi.cu", "cg_det.cu", "cg_hogwild.cu", "cg_eval.cu", "cg_modelio.cpp"]
+HEADERS = ["cg_device.cuh", "cg_kernels.h", "cg_host.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -23,6 +23,7 @@
 #include "cachegram/trainer.hpp"
 #include "cachegram_b200.h"
 #include "cg_device.cuh"
+#include "cg_host.h"
 #include "cg_kernels.h"
 
 namespace {
@@ -52,6 +53,9 @@ int guarded(F&& f) {
     } catch (const cachegram::IoError& e) {
         g_error = e.what();
         return CG_ERR_IO;
+    } catch (const cachegram::ParseError& e) {
+        g_error = e.what();
+        return CG_ERR_PARSE;
     } catch (const cachegram::NoTrainableWords& e) {
         g_error = e.what();
         return CG_ERR_NO_TRAINABLE_WORDS;
@@ -218,6 +222,8 @@ __global__ void scatter_rows_kernel(float* dst, int32_t ds, const float* src, in
 unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 }  // namespace
+
+void cgint::set_last_error(const std::string& msg) { g_error = msg; }
 
 // ============================================================================ session
 struct cg_session {
@@ -735,7 +741,8 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.dummy_row = s->V - 1;
             h.probe = s->tune.probe;
             const cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
-                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window);
+                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
+                                                     s->tune.kernel);
             // Each CTA trains its own replica of the hot rows between flushes; flushing
             // delta / n_CTA averages the replicas (local SGD + model averaging, as across
             // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every
@@ -1011,6 +1018,138 @@ int cg_cache_flush(int32_t vocab_size, int32_t dim, float* syn1, const int32_t* 
         CG_CUDA(cudaGetLastError());
         CG_CUDA(cudaMemcpy(syn1, d1.p, n1 * 4, cudaMemcpyDeviceToHost));
         CG_CUDA(cudaMemcpy(cache_flag, flag.p, static_cast<size_t>(hot_count), cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"
+
+// ============================================================================ evaluation
+struct cg_embeddings {
+    int device = 0;
+    int32_t rows = 0, dim = 0, ld = 0;
+    DevBuf<float> table;  // rows x ld, unit-normalised, zero-padded
+};
+
+namespace {
+int require_device(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    }
+    if (device < 0) {  // the calling thread's current device
+        CG_CUDA(cudaGetDevice(&device));
+        return device;
+    }
+    if (device >= ndev) invalid("device ordinal out of range");
+    CG_CUDA(cudaSetDevice(device));
+    return device;
+}
+
+int embeddings_make(const float* src, bool src_on_device, int32_t rows, int32_t dim, int32_t stride, int32_t device,
+                    cg_embeddings** out) {
+    return guarded([&] {
+        if (!out) invalid("cg_embeddings_create: out is null");
+        *out = nullptr;
+        if (rows < 0) invalid("rows must be >= 0");
+        if (dim < 1) invalid("vector dimension must be >= 1");
+        if (rows > 0 && !src) invalid("vectors is null");
+        auto e = std::make_unique<cg_embeddings>();
+        e->device = require_device(device);
+        e->rows = rows;
+        e->dim = dim;
+        e->ld = cgk::eval_ld(dim);
+        if (rows > 0) {
+            e->table.alloc(static_cast<size_t>(rows) * e->ld);
+            DevBuf<float> staged;
+            const float* dsrc = src;
+            if (!src_on_device) {
+                staged.upload(src, static_cast<size_t>(rows) * dim, nullptr);
+                dsrc = staged.p;
+            }
+            cgk::launch_normalize(dsrc, stride, e->table.p, e->ld, rows, dim, nullptr);
+            CG_CUDA(cudaGetLastError());
+            CG_CUDA(cudaDeviceSynchronize());
+        }
+        *out = e.release();
+    });
+}
+}  // namespace
+
+extern "C" {
+
+int cg_embeddings_create(const float* vectors, int32_t rows, int32_t dim, int32_t device, cg_embeddings** out) {
+    return embeddings_make(vectors, false, rows, dim, dim, device, out);
+}
+
+int cg_embeddings_create_device(const float* device_vectors, int32_t rows, int32_t dim, int32_t row_stride,
+                                int32_t device, cg_embeddings** out) {
+    if (row_stride < dim) {
+        g_error = "row_stride must be >= dim";
+        return CG_ERR_INVALID_ARGUMENT;
+    }
+    return embeddings_make(device_vectors, true, rows, dim, row_stride, device, out);
+}
+
+void cg_embeddings_destroy(cg_embeddings* e) {
+    if (!e) return;
+    cudaSetDevice(e->device);
+    delete e;
+}
+
+int32_t cg_embeddings_rows(const cg_embeddings* e) { return e ? e->rows : 0; }
+
+int cg_embeddings_normalized(const cg_embeddings* e, float* out) {
+    return guarded([&] {
+        if (!e || (!out && e->rows > 0)) invalid("null argument");
+        if (e->rows == 0) return;
+        CG_CUDA(cudaSetDevice(e->device));
+        CG_CUDA(cudaMemcpy2D(out, static_cast<size_t>(e->dim) * 4, e->table.p, static_cast<size_t>(e->ld) * 4,
+                             static_cast<size_t>(e->dim) * 4, static_cast<size_t>(e->rows), cudaMemcpyDeviceToHost));
+    });
+}
+
+int cg_analogy_answer(cg_embeddings* e, const int32_t* abc, int64_t n, int32_t* best) {
+    return guarded([&] {
+        if (!e) invalid("null embeddings");
+        if (n < 0) invalid("question count must be >= 0");
+        if (n == 0) return;
+        if (!abc || !best) invalid("null argument");
+        for (int64_t i = 0; i < 3 * n; ++i)
+            if (abc[i] < 0 || abc[i] >= e->rows) invalid("question word id out of range");
+        CG_CUDA(cudaSetDevice(e->device));
+        DevBuf<int32_t> q, out;
+        DevBuf<float> target;
+        DevBuf<unsigned long long> keys;
+        q.upload(abc, static_cast<size_t>(3 * n), nullptr);
+        out.alloc(static_cast<size_t>(n));
+        target.alloc(static_cast<size_t>(n) * e->ld);
+        keys.alloc(static_cast<size_t>(n));
+        cgk::launch_analogy(e->table.p, e->ld, e->dim, e->rows, q.p, n, target.p, keys.p, out.p, nullptr);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpy(best, out.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int cg_nearest(cg_embeddings* e, const int32_t* queries, int64_t n, int32_t k, int32_t* ids, float* scores) {
+    return guarded([&] {
+        if (!e) invalid("null embeddings");
+        if (n < 0) invalid("query count must be >= 0");
+        if (k < 1 || k > 32) invalid("k must be in [1, 32]");
+        if (n == 0) return;
+        if (!queries || !ids || !scores) invalid("null argument");
+        for (int64_t i = 0; i < n; ++i)
+            if (queries[i] < 0 || queries[i] >= e->rows) invalid("query id out of range");
+        CG_CUDA(cudaSetDevice(e->device));
+        DevBuf<int32_t> q, oid;
+        DevBuf<float> osc;
+        q.upload(queries, static_cast<size_t>(n), nullptr);
+        oid.alloc(static_cast<size_t>(n) * k);
+        osc.alloc(static_cast<size_t>(n) * k);
+        cgk::launch_topk(e->table.p, e->ld, e->rows, q.p, n, k, oid.p, osc.p, nullptr);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaMemcpy(ids, oid.p, static_cast<size_t>(n) * k * 4, cudaMemcpyDeviceToHost));
+        CG_CUDA(cudaMemcpy(scores, osc.p, static_cast<size_t>(n) * k * 4, cudaMemcpyDeviceToHost));
     });
 }
 

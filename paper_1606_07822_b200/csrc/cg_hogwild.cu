@@ -378,9 +378,264 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
     }
 }
 
+// ---- K1 v4: center-batched row groups ---------------------------------------------
+// Same persistent/ticket/flusher structure, smem layout and hot-row cache protocol as
+// hog_kernel. The difference is the per-row-group schedule: every context of a batch
+// takes its dot products against the group's rows as they were loaded (the row state at
+// the start of this center's group; within-center staleness of at most 2W updates, far
+// below the hot-row cache's own flush delay of ~64 centers), so the L x n dot products
+// of a center are independent. They are computed CI = 32/G contexts at a time and
+// reduced with one 32-value transpose-reduce (lane k ends up holding dot (k / G, k % G)),
+// each lane evaluates one sigmoid, and the updates (h_i += g U, delta += g v) follow as
+// pure FMA streams. This removes v3's serial dot -> reduce -> sigmoid -> update chain per
+// (context, group), the latency that held issue at ~46% with 12 warps per SM.
+template <int DCH, int G, int WORKERS>
+__global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) {
+    constexpr int LGG = Log2<G>::v;
+    constexpr int CI = 32 / G;  // contexts per dot chunk
+    extern __shared__ float4 hsm[];
+    float* sig = reinterpret_cast<float*>(hsm);
+    int* codes_all = reinterpret_cast<int*>(hsm + 256);
+    float4* dblk = hsm + 256 + WORKERS * (kCodeSlots / 4);
+    const int K = a.cache_rows;
+    const int d4 = a.d4;
+    int* locks = reinterpret_cast<int*>(dblk + K * d4);
+    float4* ctx_all = reinterpret_cast<float4*>(locks + ((K + 3) & ~3));
+    const int NB = a.ctx_batch;
+    __shared__ int s_done;
+    __shared__ unsigned s_merged;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int workers = (blockDim.x >> 5) - 1;
+    for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
+    for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
+    for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
+    if (tid == 0) {
+        s_done = 0;
+        s_merged = 0;
+    }
+    __syncthreads();
+
+    if (warp == workers) {  // flusher, as in hog_kernel
+        unsigned last = 0;
+        for (;;) {
+            const bool done = *reinterpret_cast<volatile int*>(&s_done) == workers;
+            const unsigned merged = *reinterpret_cast<volatile unsigned*>(&s_merged);
+            if (K > 0 && (done || merged - last >= static_cast<unsigned>(a.flush_centers))) {
+                last = merged;
+                for (int r = 0; r < K; ++r) {
+                    if (lane == 0)
+                        while (atomicCAS(&locks[r], 0, 1) != 0) {
+                        }
+                    __syncwarp();
+                    __threadfence_block();
+                    float4 d[DCH];
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        d[k] = f4(0.f);
+                        if (q < d4) {
+                            d[k] = dblk[r * d4 + q];
+                            dblk[r * d4 + q] = f4(0.f);
+                        }
+                    }
+                    __threadfence_block();
+                    __syncwarp();
+                    if (lane == 0) atomicExch(&locks[r], 0);
+                    const float sc = a.row_scale ? a.row_scale[r] : a.hot_flush_scale;
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        if (q < d4 && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
+                    }
+                }
+                __threadfence();
+            }
+            if (done) break;
+            __nanosleep(2000);
+        }
+        return;
+    }
+
+    int* codes = codes_all + warp * kCodeSlots;
+    float4* V = ctx_all + static_cast<size_t>(warp) * 2 * NB * d4;
+    float4* Hs = V + NB * d4;
+    const int dummy_code = a.dummy_row << 1;
+    const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
+    const int cpw = a.centers_per_warp;
+    const int my_g = lane & (G - 1), my_i = lane >> LGG;
+    unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
+
+    for (;;) {
+        long long c0 = 0;
+        if (lane == 0) c0 = static_cast<long long>(atomicAdd(a.counters, static_cast<unsigned long long>(cpw)));
+        c0 = __shfl_sync(kFull, c0, 0);
+        if (c0 >= n_kept) break;
+        const int64_t cend = min(static_cast<int64_t>(c0) + cpw, n_kept);
+        for (int64_t ci = c0; ci < cend; ++ci) {
+            const int32_t c = a.kept[ci];
+            const int64_t s_lo = ci / kSentence * kSentence;
+            const int64_t s_hi = min(s_lo + kSentence, n_kept);
+            const float alpha = a.sent_alpha[ci / kSentence];
+            const int b = a.window - static_cast<int>(ctr_draw(a.win_key, static_cast<uint64_t>(ci)) %
+                                                      static_cast<uint64_t>(a.window));
+            const int64_t lo = max(s_lo, ci - b), hi = min(s_hi - 1, ci + b);
+            ++n_centers;
+            const int n = static_cast<int>(hi - lo);
+            if (n == 0) continue;
+            const int p0 = a.path_off[c];
+            const int L = a.path_off[c + 1] - p0;
+            __syncwarp();
+            for (int j = lane; j < kCodeSlots; j += 32) codes[j] = j < L ? a.path_code[p0 + j] : dummy_code;
+            bool touched_cache = false;
+
+            for (int q0 = 0; q0 < n; q0 += NB) {
+                const int nb = min(NB, n - q0);
+                for (int i = 0; i < nb; ++i) {
+                    int64_t pos = lo + q0 + i;
+                    pos += pos >= ci;
+                    const int xo = a.kept[pos] * d4;
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        if (q < d4) {
+                            V[i * d4 + q] = ld_cg4(a.syn0 + 4 * (xo + q));
+                            Hs[i * d4 + q] = f4(0.f);
+                        }
+                    }
+                }
+                __syncwarp();
+                for (int j0 = 0; j0 < L; j0 += G) {
+                    float4 U[G][DCH], Dl[G][DCH];
+                    int row[G];
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        row[g] = codes[j0 + g] >> 1;
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            float4 u = f4(0.f);
+                            if (q < d4) {
+                                const int e = row[g] * d4 + q;
+                                u = row[g] < K ? add4(ld_ca4(a.syn1 + 4 * e), dblk[e]) : ld_cg4(a.syn1 + 4 * e);
+                            }
+                            U[g][k] = u;
+                            Dl[g][k] = f4(0.f);
+                        }
+                    }
+                    const int code = codes[j0 + my_g];
+                    const float turn = static_cast<float>(code & 1);
+                    const bool row_live = j0 + my_g < L;
+                    for (int cc = 0; cc < nb; cc += CI) {
+                        float p[32];
+#pragma unroll
+                        for (int ii = 0; ii < CI; ++ii) {
+                            const int i = min(cc + ii, nb - 1);  // padded contexts are masked below
+                            float4 v[DCH];
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
+                            }
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                float acc = 0.f;
+#pragma unroll
+                                for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
+                                p[ii * G + g] = acc;
+                            }
+                        }
+                        const float tot = transpose_reduce<32>(p, lane);
+                        const float f = table_sigmoid(sig, tot, a.sig_scale);
+                        const float gl = (row_live && cc + my_i < nb) ? (1.0f - turn - f) * alpha : 0.f;
+#pragma unroll
+                        for (int ii = 0; ii < CI; ++ii) {
+                            if (cc + ii >= nb) break;
+                            const int i = cc + ii;
+                            float4 v[DCH], hacc[DCH];
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
+                                hacc[k] = f4(0.f);
+                            }
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                const float gg = __shfl_sync(kFull, gl, ii * G + g);
+#pragma unroll
+                                for (int k = 0; k < DCH; ++k) {
+                                    hacc[k] = axpy4(gg, U[g][k], hacc[k]);
+                                    Dl[g][k] = axpy4(gg, v[k], Dl[g][k]);
+                                }
+                            }
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (q < d4) Hs[i * d4 + q] = add4(Hs[i * d4 + q], hacc[k]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        if (j0 + g >= L) continue;
+                        if (row[g] < K) {
+                            touched_cache = true;
+                            if (lane == 0)
+                                while (atomicCAS(&locks[row[g]], 0, 1) != 0) {
+                                }
+                            __syncwarp();
+                            __threadfence_block();
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (q < d4) {
+                                    const int e = row[g] * d4 + q;
+                                    dblk[e] = add4(dblk[e], Dl[g][k]);
+                                }
+                            }
+                            __threadfence_block();
+                            __syncwarp();
+                            if (lane == 0) atomicExch(&locks[row[g]], 0);
+                        } else if (!(a.probe & 1)) {
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (q < d4) red_add4(a.syn1 + 4 * (row[g] * d4 + q), Dl[g][k]);
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (!(a.probe & 2)) {
+                    for (int i = 0; i < nb; ++i) {
+                        int64_t pos = lo + q0 + i;
+                        pos += pos >= ci;
+                        const int xo = a.kept[pos] * d4;
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) {
+                            const int q = lane + 32 * k;
+                            if (q < d4) red_add4(a.syn0 + 4 * (xo + q), Hs[i * d4 + q]);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            n_pairs += static_cast<unsigned long long>(n);
+            n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
+            if (lane == 0 && touched_cache) atomicAdd(&s_merged, 1u);
+        }
+    }
+    if (lane == 0) {
+        atomicAdd(a.counters + 1, n_pairs);
+        atomicAdd(a.counters + 2, n_steps);
+        atomicAdd(a.counters + 3, n_centers);
+        atomicAdd(&s_done, 1);
+    }
+}
+
 template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = hog_kernel<DCH, G, WORKERS>;
+    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : hog4_kernel<DCH, 4, WORKERS>;  // v4: G = 4, CI = 8
     if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
@@ -427,8 +682,9 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
 int hog_hmax(int) { return 1 << 30; }
 
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window) {
+                     int rows_override, int window, int kernel) {
     HogGeometry g{};
+    g.kernel = kernel == 3 ? 3 : 4;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

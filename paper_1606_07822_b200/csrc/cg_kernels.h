@@ -124,13 +124,27 @@ struct HogGeometry {
     int cache_rows;
     int ctx_batch;  // contexts staged per warp
     int variant;    // DCH
+    int kernel;     // 4 = hog4_kernel (default), 3 = hog_kernel
     size_t smem;
 };
 // Depth limit on cached hot rows for this row width (none for the row-major kernel).
 int hog_hmax(int d4);
 // Picks the kernel variant for d4 and the launch geometry for the device.
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window);
+                     int rows_override, int window, int kernel);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
+
+// ---------------- evaluation (cg_eval.cu) -----------------------------------------
+// Row stride of a normalised table: dim rounded up to the scoring kernels' k-chunk.
+int eval_ld(int dim);
+// dst[r] = src[r] / sqrtf(dot(src[r], src[r])) (zeros unless the norm is > 0), rows padded to ld.
+void launch_normalize(const float* src, int64_t src_ld, float* dst, int ld, int64_t rows, int dim, cudaStream_t s);
+// 3CosAdd answers of nq questions abc[3*q..] over the first nw rows of N; T [nq*ld] and
+// best [nq] are scratch.
+void launch_analogy(const float* N, int ld, int dim, int64_t nw, const int32_t* abc, int64_t nq, float* T,
+                    unsigned long long* best, int32_t* out, cudaStream_t s);
+// Cosine top-k (k <= 32) of rows qidx[0..nq) against rows [0, nw), self excluded.
+void launch_topk(const float* N, int ld, int64_t nw, const int32_t* qidx, int64_t nq, int k, int32_t* ids,
+                 float* scores, cudaStream_t s);
 
 }  // namespace cgk

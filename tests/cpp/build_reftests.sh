@@ -12,7 +12,7 @@ REF=${REF_TESTS:-/root/reference/proj/tests}
 OUT="$HERE/_reftests"
 mkdir -p "$OUT"
 CXX=${CXX:-g++}
-for t in trainer_test huffman_test corpus_test; do
+for t in trainer_test huffman_test corpus_test model_test eval_test bench_test; do
   $CXX -std=gnu++20 -O2 -I"$ROOT/include" -I"$HERE/gtest_shim" "$REF/$t.cpp" -o "$OUT/$t" \
       -L"$ROOT/paper_1606_07822_b200" -lcachegram_b200 \
       -Wl,-rpath,"$ROOT/paper_1606_07822_b200" -Wl,-rpath,'$ORIGIN/../../../paper_1606_07822_b200'

@@ -163,6 +163,11 @@ bool almost_equal(F a, F b) {
 #define ASSERT_GE(a, b) GSHIM_ASSERT((a) >= (b), "ASSERT_GE(" #a ", " #b ")")
 #define ASSERT_LE(a, b) GSHIM_ASSERT((a) <= (b), "ASSERT_LE(" #a ", " #b ")")
 
+#define FAIL() return ::gshim::Fatal() = ::gshim::Reporter(false, __FILE__, __LINE__, "FAIL()")
+#define ADD_FAILURE() GSHIM_CHECK(false, "ADD_FAILURE()")
+#define ASSERT_NE(a, b) GSHIM_ASSERT((a) != (b), "ASSERT_NE(" #a ", " #b ")")
+#define ASSERT_LT(a, b) GSHIM_ASSERT((a) < (b), "ASSERT_LT(" #a ", " #b ")")
+#define ASSERT_GT(a, b) GSHIM_ASSERT((a) > (b), "ASSERT_GT(" #a ", " #b ")")
 #define GTEST_SKIP() return ::gshim::Fatal() = (::gshim::skipped() = true, ::gshim::Skip())
 
 int main(int, char**) {

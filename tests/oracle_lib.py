@@ -78,6 +78,10 @@ def oracle() -> C.CDLL:
         lib.orc_sample_pairs.restype = C.c_int64
         lib.orc_sample_pairs.argtypes = [P(C.c_int32), C.c_int64, P(C.c_float), C.c_int32, C.c_uint64, C.c_int64,
                                          P(C.c_int32), P(C.c_int32)]
+        lib.orc_normalize.argtypes = [P(C.c_float), C.c_int64, C.c_int32, P(C.c_float)]
+        lib.orc_analogy.argtypes = [P(C.c_float), C.c_int64, C.c_int32, P(C.c_int32), C.c_int64, P(C.c_int32)]
+        lib.orc_topk.argtypes = [P(C.c_float), C.c_int64, C.c_int32, P(C.c_int32), C.c_int64, C.c_int32,
+                                 P(C.c_int32), P(C.c_float)]
         _orc = lib
     return _orc
 
@@ -126,6 +130,13 @@ def ref() -> C.CDLL:
         lib.ref_train_center.argtypes = [P(C.c_int64), C.c_int32, C.c_int32, P(C.c_float), P(C.c_float), C.c_int32,
                                          C.c_int32, C.c_int32, P(C.c_int32), C.c_int64, C.c_int64, C.c_int32,
                                          C.c_float, C.c_int32, C.c_float]
+        lib.ref_analogy.restype = C.c_int
+        lib.ref_analogy.argtypes = [P(C.c_float), C.c_int32, C.c_int32, C.c_int32, P(C.c_int32), C.c_int64,
+                                    P(C.c_int32)]
+        lib.ref_model_save.restype = C.c_int
+        lib.ref_model_save.argtypes = [C.c_char_p, C.c_int32, C.c_char_p, P(C.c_float), C.c_int32, C.c_int32]
+        lib.ref_model_load.restype = C.c_int
+        lib.ref_model_load.argtypes = [C.c_char_p, C.c_int32, P(C.c_int32), P(C.c_int32), P(C.c_float), C.c_int64]
         _ref = lib
     return _ref
 
@@ -269,3 +280,61 @@ def max_relative_diff(a: np.ndarray, b: np.ndarray) -> float:
         return 0.0
     den = np.maximum(np.maximum(np.abs(a), np.abs(b)), 1e-2)
     return float(np.max(np.abs(a - b) / den))
+
+
+# ---------------------------------------------------------------- evaluation oracle
+def orc_normalize(vectors: np.ndarray) -> np.ndarray:
+    v = np.ascontiguousarray(vectors, dtype=np.float32)
+    out = np.empty_like(v)
+    oracle().orc_normalize(_p(v, C.c_float), v.shape[0], v.shape[1], _p(out, C.c_float))
+    return out
+
+
+def orc_analogy(norm: np.ndarray, abc: np.ndarray) -> np.ndarray:
+    n = np.ascontiguousarray(norm, dtype=np.float32)
+    q = np.ascontiguousarray(abc, dtype=np.int32).reshape(-1, 3)
+    out = np.empty(q.shape[0], np.int32)
+    oracle().orc_analogy(_p(n, C.c_float), n.shape[0], n.shape[1], _p(q, C.c_int32), q.shape[0], _p(out, C.c_int32))
+    return out
+
+
+def orc_topk(norm: np.ndarray, queries: np.ndarray, k: int):
+    n = np.ascontiguousarray(norm, dtype=np.float32)
+    q = np.ascontiguousarray(queries, dtype=np.int32)
+    ids = np.empty((q.size, k), np.int32)
+    sc = np.empty((q.size, k), np.float32)
+    oracle().orc_topk(_p(n, C.c_float), n.shape[0], n.shape[1], _p(q, C.c_int32), q.size, k, _p(ids, C.c_int32),
+                      _p(sc, C.c_float))
+    return ids, sc
+
+
+def ref_analogy(vectors: np.ndarray, restrict_top: int, abc: np.ndarray) -> np.ndarray:
+    v = np.ascontiguousarray(vectors, dtype=np.float32)
+    q = np.ascontiguousarray(abc, dtype=np.int32).reshape(-1, 3)
+    out = np.empty(q.shape[0], np.int32)
+    rc = ref().ref_analogy(_p(v, C.c_float), v.shape[0], v.shape[1], restrict_top, _p(q, C.c_int32), q.shape[0],
+                           _p(out, C.c_int32))
+    assert rc == 0, ref().ref_last_error()
+    return out
+
+
+def eval_case(seed: int, rows: int, dim: int, nq: int, dup: int = 0, zero: int = 0, nan: int = 0):
+    """Seeded embeddings with planted hazards for the analogy/top-k parity cases:
+    `dup` duplicated rows (exact score ties), `zero` all-zero rows and `nan` rows holding
+    a NaN (both normalise to zero rows, so their scores are exactly 0), plus as many rows
+    holding an inf (normalised to a NaN entry: their scores are NaN). Questions are
+    random distinct triples, plus a few with repeated words."""
+    rng = np.random.default_rng(seed)
+    v = (rng.random((rows, dim), dtype=np.float32) - 0.5).astype(np.float32)
+    for i in range(dup):
+        v[rng.integers(rows)] = v[rng.integers(rows)]
+    for i in range(zero):
+        v[rng.integers(rows)] = 0.0
+    for i in range(nan):
+        v[rng.integers(rows), rng.integers(dim)] = np.nan
+        v[rng.integers(rows), rng.integers(dim)] = np.inf  # inf / inf -> a NaN entry, NaN scores
+    abc = rng.integers(0, rows, size=(nq, 3)).astype(np.int32)
+    if nq >= 4:
+        abc[0, 1] = abc[0, 0]
+        abc[1, 2] = abc[1, 0]
+    return v, abc

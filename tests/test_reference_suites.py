@@ -38,3 +38,26 @@ def test_reference_trainer_suite_on_dropin():
     (workers = 1 -> deterministic device mode, workers = 3 -> Hogwild)."""
     out = run("trainer_test")
     assert "[==========] 20 tests" in out
+
+
+def test_reference_model_suite_on_dropin():
+    """model_test.cpp: init bits, sigmoid table, and the model files (text/binary round
+    trips, auto-detection, malformed/truncated/mismatched inputs) -- host code."""
+    out = run("model_test")
+    assert "[==========] 14 tests" in out
+
+
+@pytest.mark.gpu
+def test_reference_eval_suite_on_dropin():
+    """eval_test.cpp: question parsing, 3CosAdd answers (exact ties, exclusions,
+    restrict_top), evaluate() reports, and a train -> save -> load -> answer pipeline."""
+    out = run("eval_test")
+    assert "[==========] 15 tests" in out
+
+
+@pytest.mark.gpu
+def test_reference_bench_suite_on_dropin():
+    """bench_test.cpp: run_bench grid order, words/s consistency, accuracy column, failing
+    cells, CSV schema."""
+    out = run("bench_test")
+    assert "[==========] 6 tests" in out

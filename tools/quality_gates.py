@@ -52,6 +52,7 @@ def main():
     p.add_argument("--k", type=int, default=31)
     p.add_argument("--pairs", type=int, default=1 << 20)
     p.add_argument("--out", default="")
+    p.add_argument("--kernel", type=int, default=0, help="K1 version (0 = default)")
     a = p.parse_args()
     results = []
     threads = bench.cpu_threads()
@@ -70,7 +71,16 @@ def main():
         sel = api.select_cached_nodes(tree, a.k)
         cfg = dict(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=c.iterations,
                    cache_nodes=a.k, flush_interval=10, seed=c.seed)
-        gpu = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg, mode="hogwild"))
+        tcfg = api.TrainConfig(**cfg, mode="hogwild")
+        if a.kernel:
+            sess = api.Session(vocab, tree, sel, tcfg)
+            sess.tune(kernel=a.kernel)
+            sess.upload_ids(ids)
+            sess.train()
+            gpu = sess.download()
+            sess.close()
+        else:
+            gpu = api.train(ids, vocab, tree, sel, tcfg)
         with tempfile.TemporaryDirectory() as d:
             Oref, h, path, n = bench.reference_sample(c, vocab, ids, len(ids), d)
             r0, r1, words, wall = Oref.ref_train(h, path, cfg, workers=threads)
@@ -83,6 +93,9 @@ def main():
         row = {"config": name, "k": a.k, "epochs": c.iterations, "eval_pairs": int(cen.size), "loss": loss,
                "loss_rel_diff": abs(loss["gpu"] - loss["reference"]) / loss["reference"],
                "loss_gate_2pct": abs(loss["gpu"] - loss["reference"]) / loss["reference"] < 0.02,
+               # share of the reference's loss reduction (init -> trained) the GPU model achieves
+               "learning_ratio": (loss["init"] - loss["gpu"]) / (loss["init"] - loss["reference"]),
+               "kernel": a.kernel or 4,
                "reference_threads": threads, "reference_words_per_s": words / wall}
         if cluster is not None:
             sample = np.arange(vocab.size())
