@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--cache-nodes", type=int, default=31)
     p.add_argument("--sync-words", type=int, default=1_000_000, help="all-reduce interval per GPU (N > 1)")
     p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-text-max-tokens", type=int, default=20_000_000,
+                   help="also time train(corpus_path) on the corpus written as text when it has at most this many tokens")
     p.add_argument("--cpu-sample-tokens", type=int, default=0, help="reference sample size (0 = auto)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--warps", type=int, default=0)
@@ -165,6 +167,15 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm / CPU baseline
+def write_text(ids, vocab_size: int, path: str, n: int) -> None:
+    """The id stream as text: `w<id>` tokens, a newline every 1000 (what the reference reads)."""
+    words = np.array([b"w%d" % i for i in range(vocab_size)], dtype=object)
+    with open(path, "wb") as f:
+        for a in range(0, n, 1_000_000):
+            toks = words[ids[a:min(n, a + 1_000_000)]]
+            f.write(b"\n".join(b" ".join(toks[i:i + 1000].tolist()) for i in range(0, toks.size, 1000)) + b"\n")
+
+
 def reference_sample(c, vocab, ids, sample_tokens: int, workdir: str):
     """Writes the first `sample_tokens` tokens of the id stream as text (`w<id>`, newline
     every 1000) for the reference's file-based train(); its vocabulary is built from the
@@ -177,11 +188,7 @@ def reference_sample(c, vocab, ids, sample_tokens: int, workdir: str):
     n = min(sample_tokens, len(ids))
     ids = host_ids(ids, n)
     path = os.path.join(workdir, f"ref_sample_{c.name}.txt")
-    words = np.array([b"w%d" % i for i in range(vocab.size())], dtype=object)
-    with open(path, "wb") as f:
-        for a in range(0, n, 1_000_000):
-            toks = words[ids[a:min(n, a + 1_000_000)]]
-            f.write(b"\n".join(b" ".join(toks[i:i + 1000].tolist()) for i in range(0, toks.size, 1000)) + b"\n")
+    write_text(ids, vocab.size(), path, n)
     counts = np.ascontiguousarray(vocab.counts, np.int64)
     h = O.ref().ref_open_counts(counts.ctypes.data_as(C.POINTER(C.c_int64)), counts.size)
     return O, h, path, n
@@ -389,6 +396,27 @@ def main():
                "note": ("cg_train()" if world == 1 else "api.Session + ReplicaTrainer") +
                        ": host ids -> device, model init, subsample + train, device -> host model"}
 
+    # end to end through the drop-in train(corpus_path, ...): the corpus as a text file
+    # (page cache), tokenised on the GPU (cg_train_file), trained, model back on the host --
+    # the same work the reference's train() does in its timed region.
+    e2e_text = None
+    if rank == 0 and world == 1 and args.e2e_steps > 0 and T <= args.e2e_text_max_tokens:
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "corpus.txt")
+            write_text(host_ids(ids), vocab.size(), path, T)
+            walls = []
+            for it in range(args.e2e_steps + 1):
+                st = api.TrainStats()
+                t0 = time.perf_counter()
+                api.train(path, vocab, tree, sel, cfg, st)
+                if it > 0:
+                    walls.append(time.perf_counter() - t0)
+                assert st.words_processed == T, (st.words_processed, T)
+            w = float(np.median(walls))
+            e2e_text = {"value": T / w, "unit": UNIT, "text_bytes_per_step": os.path.getsize(path),
+                        "d2h_bytes_per_step": int(vocab.size() * c.dim * 4 + (vocab.size() - 1) * c.dim * 4),
+                        "note": "train(corpus_path) -> cg_train_file(): text file read + GPU tokenise + train + model D2H"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -417,6 +445,7 @@ def main():
                          "kernel_ms_per_launch": per_launch_ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_text": e2e_text,
             "gpu_launches": launches["n"],
             "clocks": clk,
             "detail": {"pairs_per_step": agg["pairs"] / args.steps, "path_steps_per_step": agg["steps"] / args.steps,

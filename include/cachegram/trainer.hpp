@@ -239,7 +239,12 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
     if (mode == TrainMode::Deterministic && config.workers != 1)
         throw std::invalid_argument("deterministic mode replays the single-worker stream: set workers = 1");
 
-    const std::vector<std::int32_t> ids = read_id_stream(corpus_path, vocab);  // IoError if unreadable
+    // The corpus is tokenised on the GPU (cg_train_file): IoError if it cannot be opened.
+    std::string words;
+    for (std::int32_t w = 0; w < vocab.size(); ++w) {
+        words += vocab.word(w);
+        words.push_back('\0');
+    }
     const trainer_detail::TreeArrays ta(tree);
     std::vector<std::int64_t> counts(static_cast<std::size_t>(vocab.size()));
     for (std::int32_t w = 0; w < vocab.size(); ++w) counts[static_cast<std::size_t>(w)] = vocab.count(w);
@@ -261,9 +266,8 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
 
     Model model(vocab.size(), config.dim);
     cg_train_stats st{};
-    trainer_detail::check(cg_train(&c, static_cast<std::int32_t>(mode), &m, ids.data(),
-                                   static_cast<std::int64_t>(ids.size()), model.input_matrix().data(),
-                                   model.weight_matrix().data(), &st));
+    trainer_detail::check(cg_train_file(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(), words.data(),
+                                        model.input_matrix().data(), model.weight_matrix().data(), &st));
     if (stats) {
         stats->words_processed = st.words_processed;
         stats->wall_seconds = st.wall_seconds;

@@ -221,6 +221,24 @@ typedef struct cg_tuning {
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 
+/* ---- corpus ingest on the GPU -----------------------------
+ * The corpus file is streamed through pinned buffers into HBM and tokenised there
+ * (the reference's separators, corpus.hpp:19-21). cg_corpus_open_gpu counts every
+ * distinct token on the device and orders the vocabulary exactly like
+ * build_vocabulary_file (count descending, first occurrence on ties); the same handle
+ * works with cg_corpus_* above. cg_corpus_read_ids_gpu / cg_session_load_corpus turn a
+ * file into the in-vocabulary id stream (what ShardReader + id_of yield), the latter
+ * straight into a session's device buffer. words_nul: the session's V words, NUL-
+ * terminated, in id order. device < 0 = the calling thread's current device. */
+CG_API int cg_corpus_open_gpu(const char* path, int64_t min_count, int32_t device, cg_corpus** out);
+CG_API int cg_corpus_read_ids_gpu(const cg_corpus* c, const char* path, int32_t device, int32_t* ids,
+                                  int64_t capacity, int64_t* n_ids);
+CG_API int cg_session_load_corpus(cg_session* s, const char* path, const char* words_nul, int64_t* n_ids);
+/* cg_train with the corpus given as a file: tokenised on the device (no host id stream).
+ * stats->wall_seconds covers reading the corpus, like the reference's train(). */
+CG_API int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const char* corpus_path,
+                         const char* words_nul, float* syn0_out, float* syn1_out, cg_train_stats* stats);
+
 /* ---- evaluation (eval.hpp:88-238) ---------------------------
  * A device-resident table of unit-normalised rows, built exactly like AnalogySolver
  * (eval.hpp:91-103): row / sqrtf(dot(row, row)), zeros when the norm is not > 0.

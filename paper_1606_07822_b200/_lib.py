@@ -140,6 +140,11 @@ SIGNATURES = {
     "cg_session_download": (C.c_int, [vp, P(C.c_float), P(C.c_float)]),
     "cg_session_model_buffer": (C.c_int, [vp, P(vp), P(C.c_size_t), P(C.c_int32)]),
     "cg_session_tune": (C.c_int, [vp, P(CgTuning)]),
+    "cg_corpus_open_gpu": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, P(vp)]),
+    "cg_corpus_read_ids_gpu": (C.c_int, [vp, C.c_char_p, C.c_int32, P(C.c_int32), C.c_int64, P(C.c_int64)]),
+    "cg_session_load_corpus": (C.c_int, [vp, C.c_char_p, C.c_char_p, P(C.c_int64)]),
+    "cg_train_file": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), C.c_char_p, C.c_char_p, P(C.c_float),
+                                P(C.c_float), P(CgTrainStats)]),
     "cg_embeddings_create": (C.c_int, [P(C.c_float), C.c_int32, C.c_int32, C.c_int32, P(vp)]),
     "cg_embeddings_create_device": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(vp)]),
     "cg_embeddings_destroy": (None, [vp]),

@@ -112,11 +112,15 @@ class Vocabulary:
             self._handle = None
 
 
-def build_vocabulary_file(path: str, min_count: int) -> Vocabulary:
-    """corpus.hpp:144-170 (C++ host code in the library)."""
+def build_vocabulary_file(path: str, min_count: int, device: int | None = None) -> Vocabulary:
+    """corpus.hpp:144-170. device=None: C++ host code in the library; device=k (or -1 for
+    the current device): counted on the GPU (cg_corpus_open_gpu), same result."""
     lib = load()
     h = C.c_void_p()
-    check(lib.cg_corpus_open(str(path).encode(), int(min_count), C.byref(h)))
+    if device is None:
+        check(lib.cg_corpus_open(str(path).encode(), int(min_count), C.byref(h)))
+    else:
+        check(lib.cg_corpus_open_gpu(str(path).encode(), int(min_count), int(device), C.byref(h)))
     v = lib.cg_corpus_vocab_size(h)
     counts = np.zeros(v, dtype=np.int64)
     buf = C.create_string_buffer(int(lib.cg_corpus_word_bytes(h)) + 1)
@@ -125,12 +129,19 @@ def build_vocabulary_file(path: str, min_count: int) -> Vocabulary:
     return Vocabulary(counts, [w.decode() for w in words], int(lib.cg_corpus_total_tokens(h)), _handle=h)
 
 
-def read_id_stream(path: str, vocab: Vocabulary) -> np.ndarray:
-    """The in-vocabulary id stream of a corpus file (what ShardReader + id_of yield)."""
+def read_id_stream(path: str, vocab: Vocabulary, device: int | None = None) -> np.ndarray:
+    """The in-vocabulary id stream of a corpus file (what ShardReader + id_of yield);
+    tokenised on the GPU when `device` is given."""
     if vocab._handle is None:
         raise ValueError("vocabulary was not built from a file")
     lib = load()
     n = C.c_int64()
+    if device is not None:
+        check(lib.cg_corpus_read_ids_gpu(vocab._handle, str(path).encode(), int(device), None, 0, C.byref(n)))
+        ids = np.empty(n.value, dtype=np.int32)
+        check(lib.cg_corpus_read_ids_gpu(vocab._handle, str(path).encode(), int(device), ptr(ids, C.c_int32),
+                                         n.value, C.byref(n)))
+        return ids
     check(lib.cg_corpus_read_ids(vocab._handle, str(path).encode(), None, 0, C.byref(n)))
     ids = np.empty(n.value, dtype=np.int32)
     check(lib.cg_corpus_read_ids(vocab._handle, str(path).encode(), ptr(ids, C.c_int32), n.value, C.byref(n)))
@@ -389,17 +400,20 @@ def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelectio
     mode = resolve_mode(config)
     if mode == "deterministic" and config.workers != 1:
         raise ValueError("deterministic mode replays the single-worker stream: set workers = 1")
-    if isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__"):
-        ids = read_id_stream(str(corpus), vocab)
-    else:
-        ids = np.ascontiguousarray(np.asarray(corpus, np.int32))
     keep: list = []
     desc = model_desc(vocab, tree, selection, keep)
     cfg = config.to_c()
     m = Model(vocab.size(), config.dim)
     st = CgTrainStats()
-    check(load().cg_train(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
-                          ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
+    if isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__"):
+        # tokenised on the GPU, like the drop-in C++ train(corpus_path, ...)
+        words = b"".join(vocab.word(w).encode("utf-8", "surrogateescape") + b"\0" for w in range(vocab.size()))
+        check(load().cg_train_file(C.byref(cfg), MODES[mode], C.byref(desc), str(corpus).encode(), words,
+                                   ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
+    else:
+        ids = np.ascontiguousarray(np.asarray(corpus, np.int32))
+        check(load().cg_train(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
+                              ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
     if stats is not None:
         stats.words_processed = st.words_processed
         stats.wall_seconds = st.wall_seconds
@@ -440,6 +454,14 @@ class Session:
         ids = np.ascontiguousarray(ids, np.int32)
         check(load().cg_session_upload_ids(self._h, ptr(ids, C.c_int32), ids.size))
         self.n_ids = int(ids.size)
+
+    def load_corpus(self, path: str, vocab: Vocabulary) -> int:
+        """Tokenise a corpus file on the GPU straight into the session's id buffer."""
+        words = b"".join(vocab.word(w).encode("utf-8", "surrogateescape") + b"\0" for w in range(vocab.size()))
+        n = C.c_int64()
+        check(load().cg_session_load_corpus(self._h, str(path).encode(), words, C.byref(n)))
+        self.n_ids = int(n.value)
+        return self.n_ids
 
     def upload_ids_device(self, ids_tensor) -> None:
         """Device-to-device copy of a CUDA int32 tensor of vocabulary ids."""

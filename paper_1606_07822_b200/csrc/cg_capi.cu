@@ -565,6 +565,29 @@ void cg_session_destroy(cg_session* s) {
 }
 
 namespace {
+__global__ void id_range_kernel(const int32_t* ids, int64_t n, int32_t V, unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (ids[i] < 0 || ids[i] >= V) atomicAdd(bad, 1ull);
+}
+
+// Every id must index the vocabulary (checked on the device: a host loop over 10^9 ids
+// costs a second of the end-to-end time).
+void check_ids_on_device(cg_session* s) {
+    DevBuf<unsigned long long> bad;
+    bad.alloc(1);
+    CG_CUDA(cudaMemsetAsync(bad.p, 0, 8, s->stream));
+    if (s->n_ids > 0) id_range_kernel<<<grid_for(s->n_ids), 256, 0, s->stream>>>(s->ids.p, s->n_ids, s->V, bad.p);
+    CG_CUDA(cudaGetLastError());
+    unsigned long long nbad = 0;
+    CG_CUDA(cudaMemcpyAsync(&nbad, bad.p, 8, cudaMemcpyDeviceToHost, s->stream));
+    CG_CUDA(cudaStreamSynchronize(s->stream));
+    if (nbad) {
+        s->n_ids = 0;
+        invalid("id out of vocabulary range");
+    }
+}
+
 void session_alloc_stream(cg_session* s, int64_t n_ids) {
     s->n_ids = n_ids;
     if (s->mode == CG_MODE_HOGWILD) {
@@ -581,11 +604,9 @@ int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids) {
     return guarded([&] {
         if (n_ids < 0) invalid("negative id count");
         CG_CUDA(cudaSetDevice(s->device));
-        for (int64_t i = 0; i < n_ids; ++i)
-            if (ids[i] < 0 || ids[i] >= s->V) invalid("id out of vocabulary range");
         s->ids.upload(ids, static_cast<size_t>(n_ids), s->stream);
         session_alloc_stream(s, n_ids);
-        CG_CUDA(cudaStreamSynchronize(s->stream));
+        check_ids_on_device(s);
     });
 }
 
@@ -1150,6 +1171,158 @@ int cg_nearest(cg_embeddings* e, const int32_t* queries, int64_t n, int32_t k, i
         CG_CUDA(cudaGetLastError());
         CG_CUDA(cudaMemcpy(ids, oid.p, static_cast<size_t>(n) * k * 4, cudaMemcpyDeviceToHost));
         CG_CUDA(cudaMemcpy(scores, osc.p, static_cast<size_t>(n) * k * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"
+
+// ============================================================================ GPU ingest
+namespace {
+std::vector<std::string> split_nul(const char* words_nul, int32_t n) {
+    std::vector<std::string> w(static_cast<size_t>(n));
+    const char* p = words_nul;
+    for (int32_t i = 0; i < n; ++i) {
+        w[static_cast<size_t>(i)] = p;
+        p += w[static_cast<size_t>(i)].size() + 1;
+    }
+    return w;
+}
+
+struct DevWordTable {
+    DevBuf<unsigned long long> keys;
+    DevBuf<int32_t> ids, len;
+    DevBuf<int64_t> off;
+    DevBuf<char> pool;
+    cgk::WordTableDev view{};
+    void upload(const std::vector<std::string>& words, cudaStream_t st) {
+        cgk::WordTableHost h;
+        h.build(words);
+        keys.upload(h.keys.data(), h.keys.size(), st);
+        ids.upload(h.ids.data(), h.ids.size(), st);
+        len.upload(h.len.data(), h.len.size(), st);
+        off.upload(h.off.data(), h.off.size(), st);
+        pool.upload(h.pool.data(), std::max<size_t>(h.pool.size(), 1), st);
+        if (h.pool.empty()) pool.alloc(1);
+        view = cgk::WordTableDev{keys.p, ids.p, off.p, len.p, pool.p, h.mask};
+        CG_CUDA(cudaStreamSynchronize(st));  // the host table goes out of scope
+    }
+};
+
+// Tokenises `path` on the device into `ids` (grown as needed); returns the id count.
+int64_t device_id_stream(const char* path, const std::vector<std::string>& words, int64_t hint, DevBuf<int32_t>& ids,
+                         cudaStream_t st, cgk::IngestStats* stats) {
+    DevWordTable t;
+    t.upload(words, st);
+    uint64_t cap = static_cast<uint64_t>(std::max<int64_t>(hint, 0)) + 4096;
+    for (;;) {
+        ids.alloc(cap);
+        const int64_t n = cgk::ingest_ids(path, t.view, ids.p, cap, st, stats);
+        if (static_cast<uint64_t>(n) <= cap) return n;
+        cap = static_cast<uint64_t>(n);  // the vocabulary undercounted this file: once more, exactly sized
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int cg_session_load_corpus(cg_session* s, const char* path, const char* words_nul, int64_t* n_ids) {
+    return guarded([&] {
+        if (!path || !words_nul) invalid("null argument");
+        CG_CUDA(cudaSetDevice(s->device));
+        const std::vector<std::string> words = split_nul(words_nul, s->V);
+        cgk::IngestStats ist;
+        const int64_t n = device_id_stream(path, words, s->total_tokens, s->ids, s->stream, &ist);
+        session_alloc_stream(s, n);
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+        if (n_ids) *n_ids = n;
+    });
+}
+
+int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const char* corpus_path,
+                  const char* words_nul, float* syn0_out, float* syn1_out, cg_train_stats* stats) {
+    cg_session* s = nullptr;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    int rc = cg_session_create(cfg, mode, model, dev, nullptr, &s);
+    if (rc != CG_OK) return rc;
+    const auto t0 = std::chrono::steady_clock::now();
+    rc = cg_session_load_corpus(s, corpus_path, words_nul, nullptr);
+    cg_train_stats st{};
+    if (rc == CG_OK) rc = cg_session_train(s, &st);
+    if (rc == CG_OK) rc = cg_session_download(s, syn0_out, syn1_out);
+    // like the reference's, the wall time covers reading the corpus as well as training
+    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    st.words_per_second = st.wall_seconds > 0 ? static_cast<double>(st.words_processed) / st.wall_seconds : 0.0;
+    if (stats) *stats = st;
+    cg_session_destroy(s);
+    return rc;
+}
+
+int cg_corpus_open_gpu(const char* path, int64_t min_count, int32_t device, cg_corpus** out) {
+    return guarded([&] {
+        if (!path || !out) invalid("null argument");
+        if (min_count < 1) invalid("min-count must be >= 1");
+        *out = nullptr;
+        require_device(device);
+        cudaStream_t st = nullptr;
+        CG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        std::vector<cgk::CountedWord> words;
+        try {
+            words = cgk::ingest_count(path, st, nullptr);
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaStreamDestroy(st);
+        // VocabBuilder::finish: survivors by descending count, first occurrence on ties
+        std::vector<cgk::CountedWord*> keep;
+        for (auto& w : words)
+            if (w.count >= min_count) keep.push_back(&w);
+        if (keep.empty()) throw cachegram::NoTrainableWords();
+        std::sort(keep.begin(), keep.end(), [](const cgk::CountedWord* a, const cgk::CountedWord* b) {
+            return a->count != b->count ? a->count > b->count : a->first < b->first;
+        });
+        std::vector<cachegram::VocabEntry> entries(keep.size());
+        int64_t total = 0;
+        for (size_t r = 0; r < keep.size(); ++r) {
+            entries[r].word = std::move(keep[r]->word);
+            entries[r].count = keep[r]->count;
+            total += keep[r]->count;
+        }
+        *out = new cg_corpus{cachegram::Vocabulary(std::move(entries), total)};
+    });
+}
+
+int cg_corpus_read_ids_gpu(const cg_corpus* c, const char* path, int32_t device, int32_t* ids, int64_t capacity,
+                           int64_t* n_ids) {
+    return guarded([&] {
+        if (!c || !path) invalid("null argument");
+        require_device(device);
+        std::vector<std::string> words(static_cast<size_t>(c->vocab.size()));
+        for (int32_t w = 0; w < c->vocab.size(); ++w) words[static_cast<size_t>(w)] = c->vocab.word(w);
+        cudaStream_t st = nullptr;
+        CG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        DevBuf<int32_t> dev_ids;
+        int64_t n = 0;
+        try {
+            n = device_id_stream(path, words, c->vocab.total_tokens(), dev_ids, st, nullptr);
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        if (n_ids) *n_ids = n;
+        if (ids) {
+            if (n > capacity) {
+                cudaStreamDestroy(st);
+                invalid("id buffer too small");
+            }
+            if (n) CG_CUDA(cudaMemcpyAsync(ids, dev_ids.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost, st));
+        }
+        CG_CUDA(cudaStreamSynchronize(st));
+        cudaStreamDestroy(st);
     });
 }
 

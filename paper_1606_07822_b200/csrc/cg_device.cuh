@@ -67,6 +67,15 @@ __device__ __forceinline__ void st_cg4(float* p, float4 v) {
     asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
 }
+// Asynchronous 16-byte global -> shared copy through L2 (LDGSTS, bypassing L1 like
+// ld.global.cg); completes at cp_async_wait_all().
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
 // Fire-and-forget vector atomic add at L2 (REDG.E.ADD.F32x4).
 __device__ __forceinline__ void red_add4(float* p, float4 v) {
     asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)

@@ -472,38 +472,55 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
         c0 = __shfl_sync(kFull, c0, 0);
         if (c0 >= n_kept) break;
         const int64_t cend = min(static_cast<int64_t>(c0) + cpw, n_kept);
+        // the ticket's per-center metadata in two coalesced dependent loads (lane j: center
+        // c0 + j) instead of a kept -> path_off chain per center
+        int t_p0 = 0, t_len = 0;
+        float t_alpha = 0.f;
+        if (c0 + lane < cend) {
+            const int32_t cj = a.kept[c0 + lane];
+            t_alpha = a.sent_alpha[(c0 + lane) / kSentence];
+            t_p0 = a.path_off[cj];
+            t_len = a.path_off[cj + 1] - t_p0;
+        }
         for (int64_t ci = c0; ci < cend; ++ci) {
-            const int32_t c = a.kept[ci];
+            const int jt = static_cast<int>(ci - c0);
             const int64_t s_lo = ci / kSentence * kSentence;
             const int64_t s_hi = min(s_lo + kSentence, n_kept);
-            const float alpha = a.sent_alpha[ci / kSentence];
+            const float alpha = __shfl_sync(kFull, t_alpha, jt);
+            const int p0 = __shfl_sync(kFull, t_p0, jt);
+            const int L = __shfl_sync(kFull, t_len, jt);
             const int b = a.window - static_cast<int>(ctr_draw(a.win_key, static_cast<uint64_t>(ci)) %
                                                       static_cast<uint64_t>(a.window));
             const int64_t lo = max(s_lo, ci - b), hi = min(s_hi - 1, ci + b);
             ++n_centers;
             const int n = static_cast<int>(hi - lo);
             if (n == 0) continue;
-            const int p0 = a.path_off[c];
-            const int L = a.path_off[c + 1] - p0;
             __syncwarp();
             for (int j = lane; j < kCodeSlots; j += 32) codes[j] = j < L ? a.path_code[p0 + j] : dummy_code;
             bool touched_cache = false;
 
             for (int q0 = 0; q0 < n; q0 += NB) {
                 const int nb = min(NB, n - q0);
+                // context ids in one coalesced load (lane i: context i), then every row copy
+                // of the batch in flight at once (cp.async, no registers held)
+                int xid = 0;
+                if (lane < nb) {
+                    int64_t pos = lo + q0 + lane;
+                    pos += pos >= ci;  // skip the center's own position
+                    xid = a.kept[pos];
+                }
                 for (int i = 0; i < nb; ++i) {
-                    int64_t pos = lo + q0 + i;
-                    pos += pos >= ci;
-                    const int xo = a.kept[pos] * d4;
+                    const int xo = __shfl_sync(kFull, xid, i) * d4;
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
                         if (q < d4) {
-                            V[i * d4 + q] = ld_cg4(a.syn0 + 4 * (xo + q));
+                            cp_async16(V + i * d4 + q, a.syn0 + 4 * (xo + q));
                             Hs[i * d4 + q] = f4(0.f);
                         }
                     }
                 }
+                cp_async_wait_all();
                 __syncwarp();
                 for (int j0 = 0; j0 < L; j0 += G) {
                     float4 U[G][DCH], Dl[G][DCH];
@@ -608,9 +625,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                 __syncwarp();
                 if (!(a.probe & 2)) {
                     for (int i = 0; i < nb; ++i) {
-                        int64_t pos = lo + q0 + i;
-                        pos += pos >= ci;
-                        const int xo = a.kept[pos] * d4;
+                        const int xo = __shfl_sync(kFull, xid, i) * d4;
 #pragma unroll
                         for (int k = 0; k < DCH; ++k) {
                             const int q = lane + 32 * k;
@@ -692,7 +707,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     const int workers = g.variant == 1 ? Variant<1>::WORKERS : (g.variant == 2 ? Variant<2>::WORKERS : Variant<3>::WORKERS);
     g.warps = warps_override > 0 ? std::min(warps_override, workers) : workers;
     g.blocks = blocks_override > 0 ? blocks_override : sms;
-    g.cpw = cpw_override > 0 ? cpw_override : 4;
+    g.cpw = std::min(cpw_override > 0 ? cpw_override : 4, 32);  // <= 32: a ticket's metadata is one lane each
     // shared memory: sigmoid table | path codes | hot-row cache (+locks) | context buffers
     const size_t fixed = 4096 + static_cast<size_t>(workers) * kCodeSlots * 4;
     const size_t per_row = static_cast<size_t>(d4) * 16 + 4;
@@ -703,7 +718,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     const size_t budget = 210 * 1024;
     const size_t per_ctx = static_cast<size_t>(workers) * 2 * d4 * 16;
     g.ctx_batch = static_cast<int>(std::min<size_t>(2 * static_cast<size_t>(window), (budget - fixed - cache_bytes) / per_ctx));
-    g.ctx_batch = std::max(g.ctx_batch, 1);
+    g.ctx_batch = std::min(std::max(g.ctx_batch, 1), 32);  // one context id per lane
     g.smem = fixed + cache_bytes + static_cast<size_t>(g.ctx_batch) * per_ctx;
     return g;
 }

@@ -2,6 +2,9 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
+#include <vector>
+
 #include <cuda_runtime.h>
 
 namespace cgk {
@@ -146,5 +149,65 @@ void launch_analogy(const float* N, int ld, int dim, int64_t nw, const int32_t* 
 // Cosine top-k (k <= 32) of rows qidx[0..nq) against rows [0, nw), self excluded.
 void launch_topk(const float* N, int ld, int64_t nw, const int32_t* qidx, int64_t nq, int k, int32_t* ids,
                  float* scores, cudaStream_t s);
+
+// ---------------- corpus ingest (cg_ingest.cu) ------------------------------------
+struct TokChunk {
+    const unsigned char* bytes;
+    int64_t n;
+    uint64_t global_offset;  // byte offset of bytes[0] in the file
+};
+// Vocabulary word -> id, open addressing (linear probing) on FNV-1a 64 hashes.
+struct WordTableDev {
+    const unsigned long long* keys;
+    const int32_t* ids;
+    const int64_t* off;
+    const int32_t* len;
+    const char* pool;
+    uint64_t mask;
+};
+struct WordTableHost {
+    std::vector<unsigned long long> keys;
+    std::vector<int32_t> ids;
+    std::vector<int64_t> off;
+    std::vector<int32_t> len;
+    std::vector<char> pool;
+    uint64_t mask = 0;
+    void build(const std::vector<std::string>& words);
+};
+struct CountTableDev {
+    unsigned long long* keys;
+    unsigned long long* count;
+    unsigned long long* first;  // byte offset of the first occurrence
+    unsigned long long* off;    // word bytes in pool
+    int32_t* len;
+    char* pool;
+    uint64_t pool_capacity;
+    unsigned long long* pool_cursor;
+    unsigned long long* distinct;
+    unsigned long long* overflow;
+    uint64_t mask;
+};
+struct CountEntry {
+    unsigned long long count, first, off;
+    int32_t len, pad;
+};
+struct CountedWord {
+    std::string word;
+    int64_t count;
+    uint64_t first;
+};
+struct IngestStats {
+    uint64_t bytes = 0;
+    double seconds = 0.0;
+    int32_t launches = 0;
+};
+unsigned long long host_token_hash(const char* s, size_t len);
+// Tokenises a corpus file on the device; in-vocabulary ids are written in file order to
+// out[0..capacity) (device). Returns the number of in-vocabulary tokens (which may exceed
+// capacity: then only the first `capacity` were written).
+int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, uint64_t capacity, cudaStream_t st,
+                   IngestStats* stats);
+// Counts every distinct token of a corpus file on the device (unordered).
+std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestStats* stats);
 
 }  // namespace cgk

@@ -1,0 +1,117 @@
+"""GPU corpus ingest (cg_ingest.cu) against the host implementation of the drop-in
+(build_vocabulary_file / read_id_stream, itself pinned to the reference by the
+reference's own corpus suite): the vocabulary (words, counts, order, total) and the
+in-vocabulary id stream must be identical, including separators of every kind, ties,
+OOV tokens, min_count filtering and multi-chunk files; train(corpus_path) -- which now
+tokenises on the GPU -- must stay bit-identical to the reference in deterministic mode."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import fixtures as F
+import oracle_lib as O
+from paper_1606_07822_b200 import _lib, api
+
+pytestmark = pytest.mark.gpu
+
+
+def _vocab_pair(path, min_count):
+    host = api.build_vocabulary_file(str(path), min_count)
+    gpu = api.build_vocabulary_file(str(path), min_count, device=0)
+    return host, gpu
+
+
+def _same_vocab(a, b):
+    assert a.words == b.words
+    assert np.array_equal(a.counts, b.counts)
+    assert a.total_tokens() == b.total_tokens()
+
+
+def _raw_corpus(seed, n_tokens, types, seps=(" ", "\n", "\t", "\r\n", "  ", "\x0b", "\x0c")):
+    rng = np.random.default_rng(seed)
+    ranks = np.minimum(rng.zipf(1.1, n_tokens), types) - 1
+    sep = rng.integers(0, len(seps), n_tokens)
+    parts = []
+    for r, s in zip(ranks, sep):
+        parts.append(f"t{r}" if r % 7 else f"longer_token_{r}_xyz")
+        parts.append(seps[s])
+    return "\t " + "".join(parts) + ("tail" if seed % 2 else "")
+
+
+CASES = [(1, 20000, 300, 1), (2, 50000, 2000, 2), (3, 3000, 50, 5), (4, 100000, 40000, 1)]
+
+
+@pytest.mark.parametrize("seed,n,types,min_count", CASES)
+def test_gpu_vocabulary_equals_host(tmp_path, seed, n, types, min_count):
+    p = tmp_path / "c.txt"
+    p.write_text(_raw_corpus(seed, n, types))
+    host, gpu = _vocab_pair(p, min_count)
+    _same_vocab(host, gpu)
+
+
+@pytest.mark.parametrize("seed,n,types,min_count", CASES)
+def test_gpu_id_stream_equals_host(tmp_path, seed, n, types, min_count):
+    p = tmp_path / "c.txt"
+    p.write_text(_raw_corpus(seed, n, types))
+    vocab = api.build_vocabulary_file(str(p), min_count)
+    # a vocabulary from another file: the GPU reader must drop exactly the same OOV tokens
+    q = tmp_path / "other.txt"
+    q.write_text(_raw_corpus(seed + 100, n // 2, types))
+    other = api.build_vocabulary_file(str(q), 1)
+    for v in (vocab, other):
+        assert np.array_equal(api.read_id_stream(str(p), v), api.read_id_stream(str(p), v, device=0))
+
+
+def test_reference_fixture_corpora(tmp_path):
+    for mb, types, seed in ((200 * 1024, 2000, 4242), (30000, 120, 21)):
+        p = F.write(tmp_path / "f.txt", F.make_zipf_corpus(mb, types, seed))
+        for mc in (1, 5):
+            host, gpu = _vocab_pair(p, mc)
+            _same_vocab(host, gpu)
+            assert np.array_equal(api.read_id_stream(p, host), api.read_id_stream(p, gpu, device=0))
+
+
+def test_edge_cases(tmp_path):
+    p = tmp_path / "e.txt"
+    p.write_text("")
+    with pytest.raises(_lib.CgError):  # NoTrainableWords
+        api.build_vocabulary_file(str(p), 1, device=0)
+    p.write_text(" \n\t  ")
+    with pytest.raises(_lib.CgError):
+        api.build_vocabulary_file(str(p), 1, device=0)
+    p.write_text("a b a c b a " + "x" * 100000 + " a")  # a very long token
+    host, gpu = _vocab_pair(p, 1)
+    _same_vocab(host, gpu)
+    with pytest.raises(OSError):
+        api.build_vocabulary_file("/nonexistent/corpus.txt", 1, device=0)
+
+
+def test_multi_chunk_file(tmp_path):
+    """> 2 chunks of the id reader (128 MiB) and of the counter (64 MiB)."""
+    rng = np.random.default_rng(7)
+    words = np.array([f"w{i}" for i in range(70000)])
+    p = tmp_path / "big.txt"
+    with open(p, "w") as f:
+        for _ in range(12):
+            r = np.minimum(rng.zipf(1.05, 4_000_000), 70000) - 1
+            f.write(" ".join(words[r]))
+            f.write("\n")
+    assert p.stat().st_size > 200 << 20
+    host, gpu = _vocab_pair(p, 1)
+    _same_vocab(host, gpu)
+    assert np.array_equal(api.read_id_stream(str(p), host), api.read_id_stream(str(p), host, device=0))
+
+
+def test_train_from_file_is_bit_exact(tmp_path):
+    """train(corpus_path) tokenises on the GPU; deterministic mode must equal the oracle."""
+    path = F.write(tmp_path / "t.txt", F.make_zipf_corpus(60_000, 300, 77))
+    vocab = api.build_vocabulary_file(path, 2)
+    ids = api.read_id_stream(path, vocab)
+    tree = api.build_huffman_tree(vocab)
+    sel = api.select_cached_nodes(tree, 31)
+    cfg = dict(dim=24, window=4, min_count=2, sample=1e-3, iterations=2, cache_nodes=31, flush_interval=10, seed=5)
+    m = api.train(path, vocab, tree, sel, api.TrainConfig(**cfg, mode="deterministic"))
+    s0, s1, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
+    assert np.array_equal(m.syn0.view(np.uint32), s0.view(np.uint32))
+    assert np.array_equal(m.syn1.view(np.uint32), s1.view(np.uint32))

@@ -62,6 +62,8 @@ def main():
     grids["scales"] = [dict(k=0)] + [dict(k=k, scale=sc) for k in (31, 255) for sc in (1 / 148, 1 / 64, 1 / 32, 1 / 16, 1 / 8)]
     grids["probe"] = [dict(), dict(probe=1), dict(probe=2), dict(probe=3), dict(probe=4), dict(probe=7),
                       dict(k=0, probe=1), dict(cold=1)]
+    grids["probe34"] = [dict(kernel=kn, probe=pb) for kn in (4, 3) for pb in (0, 1, 2, 4, 7)] + \
+        [dict(kernel=4, cpw=1), dict(kernel=4, cpw=16), dict(kernel=4, warps=8), dict(kernel=4, k=0)]
     grids["perf"] = [dict(), dict(cpw=1), dict(cpw=8), dict(cpw=16), dict(flush=16), dict(flush=256), dict(k=0),
                      dict(warps=8), dict(scale=1 / 16), dict(cold=1)]
     grids["default"] = [
@@ -75,7 +77,7 @@ def main():
         cfg = api.TrainConfig(**dict(cfgd, cache_nodes=k), mode="hogwild")
         s = api.Session(vocab, tree, sel, cfg)
         s.tune(g.get("blocks", 0), g.get("warps", 0), g.get("cpw", 0), -1, g.get("cold", 0), g.get("scale", 0.0),
-               g.get("flush", 0), g.get("minrows", 0), g.get("probe", 0))
+               g.get("flush", 0), g.get("minrows", 0), g.get("probe", 0), g.get("kernel", 0))
         s.upload_ids(ids)
         ms = 0.0
         for it in range(a.iterations):
