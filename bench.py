@@ -167,9 +167,9 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm / CPU baseline
-def write_text(ids, vocab_size: int, path: str, n: int) -> None:
-    """The id stream as text: `w<id>` tokens, a newline every 1000 (what the reference reads)."""
-    words = np.array([b"w%d" % i for i in range(vocab_size)], dtype=object)
+def write_text(ids, words_of_id, path: str, n: int) -> None:
+    """The id stream as text (token of id i = words_of_id[i]), a newline every 1000 tokens."""
+    words = np.array([w if isinstance(w, bytes) else w.encode() for w in words_of_id], dtype=object)
     with open(path, "wb") as f:
         for a in range(0, n, 1_000_000):
             toks = words[ids[a:min(n, a + 1_000_000)]]
@@ -188,7 +188,7 @@ def reference_sample(c, vocab, ids, sample_tokens: int, workdir: str):
     n = min(sample_tokens, len(ids))
     ids = host_ids(ids, n)
     path = os.path.join(workdir, f"ref_sample_{c.name}.txt")
-    write_text(ids, vocab.size(), path, n)
+    write_text(ids, [b"w%d" % i for i in range(vocab.size())], path, n)  # ref_open_counts names word i "w<i>"
     counts = np.ascontiguousarray(vocab.counts, np.int64)
     h = O.ref().ref_open_counts(counts.ctypes.data_as(C.POINTER(C.c_int64)), counts.size)
     return O, h, path, n
@@ -403,7 +403,7 @@ def main():
     if rank == 0 and world == 1 and args.e2e_steps > 0 and T <= args.e2e_text_max_tokens:
         with tempfile.TemporaryDirectory() as d:
             path = os.path.join(d, "corpus.txt")
-            write_text(host_ids(ids), vocab.size(), path, T)
+            write_text(host_ids(ids), [vocab.word(i) for i in range(vocab.size())], path, T)
             walls = []
             for it in range(args.e2e_steps + 1):
                 st = api.TrainStats()

@@ -50,6 +50,9 @@ int guarded(F&& f) {
     } catch (const CgError& e) {
         g_error = e.what();
         return e.code;
+    } catch (const cgint::CudaError& e) {
+        g_error = e.what();
+        return CG_ERR_CUDA;
     } catch (const cachegram::IoError& e) {
         g_error = e.what();
         return CG_ERR_IO;
@@ -102,67 +105,6 @@ void validate_model(const cg_model_desc& m) {
             invalid("cache selection was built from a different tree");
 }
 
-// Caching device allocator: train() / sessions are created per call, and cudaMalloc /
-// cudaFree of hundreds of MB per call costs 0.1-1 s on the driver. Freed blocks are kept
-// per (device, size class) and reused; sizes round up to 2 MiB (>= 1 MiB) or 256 B.
-class DevicePool {
-public:
-    static DevicePool& get() {
-        static DevicePool* p = new DevicePool();  // leaked on purpose: no teardown-order issues at exit
-        return *p;
-    }
-    void* alloc(size_t bytes) {
-        const size_t sz = round(bytes);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        {
-            std::lock_guard<std::mutex> g(mu_);
-            auto& fl = free_[{dev, sz}];
-            if (!fl.empty()) {
-                void* p = fl.back();
-                fl.pop_back();
-                return p;
-            }
-        }
-        void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, sz);
-        if (e != cudaSuccess) {  // release cached blocks and retry once
-            cudaGetLastError();
-            release();
-            e = cudaMalloc(&p, sz);
-        }
-        check_cuda(e, "cudaMalloc");
-        std::lock_guard<std::mutex> g(mu_);
-        size_of_[p] = {dev, sz};
-        return p;
-    }
-    void free(void* p) {
-        if (!p) return;
-        std::lock_guard<std::mutex> g(mu_);
-        auto it = size_of_.find(p);
-        if (it == size_of_.end()) return;
-        free_[it->second].push_back(p);
-    }
-    void release() {
-        std::lock_guard<std::mutex> g(mu_);
-        for (auto& [key, fl] : free_) {
-            for (void* p : fl) {
-                cudaFree(p);
-                size_of_.erase(p);
-            }
-            fl.clear();
-        }
-    }
-
-private:
-    static size_t round(size_t b) {
-        if (b >= (size_t{1} << 20)) return (b + (size_t{2} << 20) - 1) & ~((size_t{2} << 20) - 1);
-        return (b + 255) & ~size_t{255};
-    }
-    std::mutex mu_;
-    std::map<std::pair<int, size_t>, std::vector<void*>> free_;
-    std::map<void*, std::pair<int, size_t>> size_of_;
-};
 
 template <typename T>
 struct DevBuf {
@@ -171,12 +113,12 @@ struct DevBuf {
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    ~DevBuf() { DevicePool::get().free(p); }
+    ~DevBuf() { cgint::DevicePool::get().free(p); }
     void alloc(size_t count) {
-        DevicePool::get().free(p);
+        cgint::DevicePool::get().free(p);
         p = nullptr;
         n = count;
-        if (count) p = static_cast<T*>(DevicePool::get().alloc(count * sizeof(T)));
+        if (count) p = static_cast<T*>(cgint::DevicePool::get().alloc(count * sizeof(T)));
     }
     void upload(const T* host, size_t count, cudaStream_t s) {
         alloc(count);
@@ -321,7 +263,10 @@ extern "C" {
 
 int cg_abi_version(void) { return CG_ABI_VERSION; }
 
-void cg_release_cached_memory(void) { DevicePool::get().release(); }
+void cg_release_cached_memory(void) {
+    cgint::DevicePool::get().release();
+    cgint::PinnedPool::get().release();
+}
 const char* cg_last_error(void) { return g_error.c_str(); }
 
 int cg_device_count(void) {

@@ -379,6 +379,42 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 }
 
 // ---- K1 v4: center-batched row groups ---------------------------------------------
+// Learning signals of CIc contexts (cc .., clamped to the batch) against the G rows in U:
+// the CIc*G dot products are reduced together (transpose-reduce), after which the pair
+// (ii, g) lives in lane (ii*G + g) << (5 - log2(CIc*G)); each lane returns its pair's
+// g = (1 - turn - sigmoid(dot)) * alpha, or 0 for a padded context / row.
+template <int DCH, int G, int CIc>
+__device__ __forceinline__ float chunk_signal(const float4* V, int d4, int lane, int cc, int nb,
+                                              const float4 (&U)[G][DCH], const int* codes, int j0, int L,
+                                              const float* sig, float sig_scale, float alpha) {
+    constexpr int N = CIc * G;
+    constexpr int LN = Log2<N>::v, LGG = Log2<G>::v;
+    float p[N];
+#pragma unroll
+    for (int ii = 0; ii < CIc; ++ii) {
+        const int i = min(cc + ii, nb - 1);
+        float4 v[DCH];
+#pragma unroll
+        for (int k = 0; k < DCH; ++k) {
+            const int q = lane + 32 * k;
+            v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
+            p[ii * G + g] = acc;
+        }
+    }
+    const float tot = transpose_reduce<N>(p, lane);
+    const int vi = lane >> (5 - LN);
+    const int my_i = vi >> LGG, my_g = vi & (G - 1);
+    const int code = codes[j0 + my_g];
+    const float f = table_sigmoid(sig, tot, sig_scale);
+    return (j0 + my_g < L && cc + my_i < nb) ? (1.0f - static_cast<float>(code & 1) - f) * alpha : 0.f;
+}
+
 // Same persistent/ticket/flusher structure, smem layout and hot-row cache protocol as
 // hog_kernel. The difference is the per-row-group schedule: every context of a batch
 // takes its dot products against the group's rows as they were loaded (the row state at
@@ -391,8 +427,6 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 // (context, group), the latency that held issue at ~46% with 12 warps per SM.
 template <int DCH, int G, int WORKERS>
 __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) {
-    constexpr int LGG = Log2<G>::v;
-    constexpr int CI = 32 / G;  // contexts per dot chunk
     extern __shared__ float4 hsm[];
     float* sig = reinterpret_cast<float*>(hsm);
     int* codes_all = reinterpret_cast<int*>(hsm + 256);
@@ -460,10 +494,22 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     int* codes = codes_all + warp * kCodeSlots;
     float4* V = ctx_all + static_cast<size_t>(warp) * 2 * NB * d4;
     float4* Hs = V + NB * d4;
+    // per-warp staging of the next row group (cp.async one group ahead of its use)
+    float4* Ub = ctx_all + static_cast<size_t>(workers) * 2 * NB * d4 + static_cast<size_t>(warp) * G * d4;
+    auto prefetch_group = [&](int j0) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            const int rg = codes[j0 + g] >> 1;
+#pragma unroll
+            for (int k = 0; k < DCH; ++k) {
+                const int q = lane + 32 * k;
+                if (q < d4) cp_async16(Ub + g * d4 + q, a.syn1 + 4 * (rg * d4 + q));
+            }
+        }
+    };
     const int dummy_code = a.dummy_row << 1;
     const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
     const int cpw = a.centers_per_warp;
-    const int my_g = lane & (G - 1), my_i = lane >> LGG;
     unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
 
     for (;;) {
@@ -509,6 +555,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                     pos += pos >= ci;  // skip the center's own position
                     xid = a.kept[pos];
                 }
+                __syncwarp();  // codes visible; Ub free
+                prefetch_group(0);
                 for (int i = 0; i < nb; ++i) {
                     const int xo = __shfl_sync(kFull, xid, i) * d4;
 #pragma unroll
@@ -520,9 +568,9 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                         }
                     }
                 }
-                cp_async_wait_all();
-                __syncwarp();
                 for (int j0 = 0; j0 < L; j0 += G) {
+                    cp_async_wait_all();  // this group's rows (and, first time, the contexts)
+                    __syncwarp();
                     float4 U[G][DCH], Dl[G][DCH];
                     int row[G];
 #pragma unroll
@@ -533,41 +581,38 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                             const int q = lane + 32 * k;
                             float4 u = f4(0.f);
                             if (q < d4) {
-                                const int e = row[g] * d4 + q;
-                                u = row[g] < K ? add4(ld_ca4(a.syn1 + 4 * e), dblk[e]) : ld_cg4(a.syn1 + 4 * e);
+                                u = Ub[g * d4 + q];
+                                if (row[g] < K) u = add4(u, dblk[row[g] * d4 + q]);  // + this CTA's cached delta
                             }
                             U[g][k] = u;
                             Dl[g][k] = f4(0.f);
                         }
                     }
-                    const int code = codes[j0 + my_g];
-                    const float turn = static_cast<float>(code & 1);
-                    const bool row_live = j0 + my_g < L;
-                    for (int cc = 0; cc < nb; cc += CI) {
-                        float p[32];
-#pragma unroll
-                        for (int ii = 0; ii < CI; ++ii) {
-                            const int i = min(cc + ii, nb - 1);  // padded contexts are masked below
-                            float4 v[DCH];
-#pragma unroll
-                            for (int k = 0; k < DCH; ++k) {
-                                const int q = lane + 32 * k;
-                                v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
-                            }
-#pragma unroll
-                            for (int g = 0; g < G; ++g) {
-                                float acc = 0.f;
-#pragma unroll
-                                for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
-                                p[ii * G + g] = acc;
-                            }
+                    __syncwarp();  // every lane has its copy: Ub takes the next group
+                    if (j0 + G < L) prefetch_group(j0 + G);
+                    for (int cc = 0; cc < nb;) {
+                        // chunk of 8, 4 or 2 contexts: a center's 2b contexts (b = 1..W) are
+                        // covered without computing dots for padding (a fixed 8 wasted ~40%)
+                        const int r = nb - cc;
+                        float gl;
+                        int ls, cic;
+                        if (r >= 8) {
+                            gl = chunk_signal<DCH, G, 8>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
+                            ls = 5 - Log2<8 * G>::v;
+                            cic = 8;
+                        } else if (r >= 4) {
+                            gl = chunk_signal<DCH, G, 4>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
+                            ls = 5 - Log2<4 * G>::v;
+                            cic = 4;
+                        } else {
+                            gl = chunk_signal<DCH, G, 2>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
+                            ls = 5 - Log2<2 * G>::v;
+                            cic = 2;
                         }
-                        const float tot = transpose_reduce<32>(p, lane);
-                        const float f = table_sigmoid(sig, tot, a.sig_scale);
-                        const float gl = (row_live && cc + my_i < nb) ? (1.0f - turn - f) * alpha : 0.f;
-#pragma unroll
-                        for (int ii = 0; ii < CI; ++ii) {
-                            if (cc + ii >= nb) break;
+                        // rolled on purpose: unrolled, the kernel's hot loop outgrows the
+                        // instruction cache (ncu: 21% no_instruction stalls)
+#pragma unroll 1
+                        for (int ii = 0; ii < min(cic, r); ++ii) {
                             const int i = cc + ii;
                             float4 v[DCH], hacc[DCH];
 #pragma unroll
@@ -578,7 +623,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                             }
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
-                                const float gg = __shfl_sync(kFull, gl, ii * G + g);
+                                const float gg = __shfl_sync(kFull, gl, (ii * G + g) << ls);
 #pragma unroll
                                 for (int k = 0; k < DCH; ++k) {
                                     hacc[k] = axpy4(gg, U[g][k], hacc[k]);
@@ -591,6 +636,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                                 if (q < d4) Hs[i * d4 + q] = add4(Hs[i * d4 + q], hacc[k]);
                             }
                         }
+                        cc += cic;
                     }
 #pragma unroll
                     for (int g = 0; g < G; ++g) {
@@ -715,11 +761,33 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     if (rows_override >= 0 && rows_override < rows) rows = rows_override;
     g.cache_rows = std::max(rows, 0);
     const size_t cache_bytes = static_cast<size_t>(g.cache_rows) * d4 * 16 + static_cast<size_t>((g.cache_rows + 3) & ~3) * 4;
-    const size_t budget = 210 * 1024;
-    const size_t per_ctx = static_cast<size_t>(workers) * 2 * d4 * 16;
-    g.ctx_batch = static_cast<int>(std::min<size_t>(2 * static_cast<size_t>(window), (budget - fixed - cache_bytes) / per_ctx));
-    g.ctx_batch = std::min(std::max(g.ctx_batch, 1), 32);  // one context id per lane
-    g.smem = fixed + cache_bytes + static_cast<size_t>(g.ctx_batch) * per_ctx;
+    // v4 also stages each warp's next row group (4 rows) in shared memory. A center whose
+    // 2b contexts do not fit one context batch re-reads (and re-writes) its whole path per
+    // batch, which costs more than a worker warp: unless the caller fixed the warp count,
+    // drop up to 3 warps if that lets one batch hold a full window (2W contexts).
+    const size_t budget = 225 * 1024;
+    auto batch_for = [&](int warps, size_t* smem) {
+        const size_t prefetch = g.kernel == 4 ? static_cast<size_t>(warps) * 4 * d4 * 16 : 0;
+        const size_t per_ctx = static_cast<size_t>(warps) * 2 * d4 * 16;
+        const size_t room = budget > fixed + cache_bytes + prefetch ? budget - fixed - cache_bytes - prefetch : 0;
+        int nb = static_cast<int>(std::min<size_t>(2 * static_cast<size_t>(window), room / per_ctx));
+        nb = std::min(std::max(nb, 1), 32);  // one context id per lane
+        *smem = fixed + cache_bytes + prefetch + static_cast<size_t>(nb) * per_ctx;
+        return nb;
+    };
+    g.ctx_batch = batch_for(g.warps, &g.smem);
+    if (warps_override <= 0 && g.ctx_batch < 2 * window) {
+        for (int w = g.warps - 1; w >= std::max(1, g.warps - 3); --w) {
+            size_t sm = 0;
+            const int nb = batch_for(w, &sm);
+            if (nb >= 2 * window) {
+                g.warps = w;
+                g.ctx_batch = nb;
+                g.smem = sm;
+                break;
+            }
+        }
+    }
     return g;
 }
 

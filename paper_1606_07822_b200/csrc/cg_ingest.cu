@@ -34,6 +34,7 @@
 
 #include "cachegram/errors.hpp"
 #include "cg_device.cuh"
+#include "cg_host.h"
 #include "cg_kernels.h"
 
 namespace cgk {
@@ -268,7 +269,20 @@ __global__ void fill_u64_kernel(unsigned long long* p, uint64_t n, unsigned long
 }
 
 void check(cudaError_t e, const char* what) {
-    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    if (e != cudaSuccess) throw cgint::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Device / pinned buffers come from the library's caching pools: the ingest runs once per
+// train(corpus_path) call, and raw cudaMalloc/cudaMallocHost of ~0.5 GB per call would
+// cost more than the tokenisation itself.
+template <typename T>
+void dalloc(T** p, size_t bytes) {
+    *p = static_cast<T*>(cgint::DevicePool::get().alloc(bytes));
+}
+template <typename T>
+void dfree(T*& p) {
+    cgint::DevicePool::get().free(p);
+    p = nullptr;
 }
 
 unsigned grid_of(uint64_t n) { return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148ull * 16)); }
@@ -280,12 +294,11 @@ public:
     ChunkReader(const char* path, size_t chunk) : cap_(chunk) {
         f_ = std::fopen(path, "rb");
         if (!f_) throw cachegram::IoError(std::string("cannot open corpus file: ") + path);
-        for (auto& b : buf_) check(cudaMallocHost(&b, cap_), "cudaMallocHost");
+        for (auto& b : buf_) b = static_cast<unsigned char*>(cgint::PinnedPool::get().alloc(cap_));
     }
     ~ChunkReader() {
         if (f_) std::fclose(f_);
-        for (auto* b : buf_)
-            if (b) cudaFreeHost(b);
+        for (auto* b : buf_) cgint::PinnedPool::get().free(b);
     }
     // Fills buffer `which`; returns the usable length (0 at the end of the file).
     size_t next(int which) {
@@ -318,10 +331,9 @@ private:
     void grow(int which, size_t have) {
         const size_t ncap = cap_ * 2;
         for (int k = 0; k < 2; ++k) {
-            unsigned char* nb = nullptr;
-            check(cudaMallocHost(&nb, ncap), "cudaMallocHost");
+            unsigned char* nb = static_cast<unsigned char*>(cgint::PinnedPool::get().alloc(ncap));
             if (k == which) std::memcpy(nb, buf_[k], have);
-            cudaFreeHost(buf_[k]);
+            cgint::PinnedPool::get().free(buf_[k]);
             buf_[k] = nb;
         }
         cap_ = ncap;
@@ -394,19 +406,19 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
         if (bytes <= dcap) return;
         check(cudaStreamSynchronize(st), "sync");
         for (auto& p : dbytes) {
-            cudaFree(p);
-            check(cudaMalloc(&p, bytes + 16), "cudaMalloc");
+            dfree(p);
+            dalloc(&p, bytes + 16);
         }
-        cudaFree(tmp);
-        cudaFree(tcount);
-        cudaFree(toff);
+        dfree(tmp);
+        dfree(tcount);
+        dfree(toff);
         const size_t nt = (bytes + kTokTile - 1) / kTokTile;
-        check(cudaMalloc(&tmp, nt * kTokCap * sizeof(int32_t)), "cudaMalloc");
-        check(cudaMalloc(&tcount, nt * sizeof(uint32_t)), "cudaMalloc");
-        check(cudaMalloc(&toff, (nt + 1) * sizeof(uint64_t)), "cudaMalloc");
+        dalloc(&tmp, nt * kTokCap * sizeof(int32_t));
+        dalloc(&tcount, nt * sizeof(uint32_t));
+        dalloc(&toff, (nt + 1) * sizeof(uint64_t));
         dcap = bytes;
     };
-    check(cudaMalloc(&cursor, sizeof(uint64_t)), "cudaMalloc");
+    dalloc(&cursor, sizeof(uint64_t));
     check(cudaMemsetAsync(cursor, 0, sizeof(uint64_t), st), "memset");
     for (auto& e : done) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     bool used[2] = {false, false};
@@ -436,11 +448,11 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
         check(cudaMemcpyAsync(&total, cursor, sizeof total, cudaMemcpyDeviceToHost, st), "D2H");
         check(cudaStreamSynchronize(st), "sync");
         for (auto& e : done) cudaEventDestroy(e);
-        for (auto* p : dbytes) cudaFree(p);
-        cudaFree(tmp);
-        cudaFree(tcount);
-        cudaFree(toff);
-        cudaFree(cursor);
+        for (auto*& p : dbytes) dfree(p);
+        dfree(tmp);
+        dfree(tcount);
+        dfree(toff);
+        dfree(cursor);
         if (stats) {
             stats->bytes = bytes_total;
             stats->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -449,11 +461,11 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
     } catch (...) {
         cudaStreamSynchronize(st);
         for (auto& e : done) cudaEventDestroy(e);
-        for (auto* p : dbytes) cudaFree(p);
-        cudaFree(tmp);
-        cudaFree(tcount);
-        cudaFree(toff);
-        cudaFree(cursor);
+        for (auto*& p : dbytes) dfree(p);
+        dfree(tmp);
+        dfree(tcount);
+        dfree(toff);
+        dfree(cursor);
         throw;
     }
 }
@@ -465,22 +477,22 @@ struct DevCountTable {
     void alloc(uint64_t slots, cudaStream_t st) {
         cap = slots;
         t.mask = slots - 1;
-        check(cudaMalloc(&t.keys, slots * 8), "cudaMalloc");
-        check(cudaMalloc(&t.count, slots * 8), "cudaMalloc");
-        check(cudaMalloc(&t.first, slots * 8), "cudaMalloc");
-        check(cudaMalloc(&t.off, slots * 8), "cudaMalloc");
-        check(cudaMalloc(&t.len, slots * 4), "cudaMalloc");
+        dalloc(&t.keys, slots * 8);
+        dalloc(&t.count, slots * 8);
+        dalloc(&t.first, slots * 8);
+        dalloc(&t.off, slots * 8);
+        dalloc(&t.len, slots * 4);
         check(cudaMemsetAsync(t.keys, 0, slots * 8, st), "memset");
         check(cudaMemsetAsync(t.count, 0, slots * 8, st), "memset");
         fill_u64_kernel<<<grid_of(slots), 256, 0, st>>>(t.first, slots, ~0ull);
         fill_u64_kernel<<<grid_of(slots), 256, 0, st>>>(t.off, slots, kUnpublished);
     }
     void release() {
-        cudaFree(t.keys);
-        cudaFree(t.count);
-        cudaFree(t.first);
-        cudaFree(t.off);
-        cudaFree(t.len);
+        dfree(t.keys);
+        dfree(t.count);
+        dfree(t.first);
+        dfree(t.off);
+        dfree(t.len);
         t.keys = t.count = t.first = t.off = nullptr;
         t.len = nullptr;
     }
@@ -502,13 +514,13 @@ std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestS
     auto cleanup = [&] {
         cudaStreamSynchronize(st);
         for (auto& e : done) cudaEventDestroy(e);
-        for (auto* p : dbytes) cudaFree(p);
+        for (auto*& p : dbytes) dfree(p);
         tab.release();
-        cudaFree(scalars);
-        cudaFree(pool);
+        dfree(scalars);
+        dfree(pool);
     };
     try {
-        check(cudaMalloc(&scalars, 4 * 8), "cudaMalloc");
+        dalloc(&scalars, 4 * 8);
         check(cudaMemsetAsync(scalars, 0, 4 * 8, st), "memset");
         uint64_t distinct_bound = 0;  // upper bound on distinct words so far
         uint64_t pool_bound = 0;      // upper bound on pool bytes so far
@@ -522,8 +534,8 @@ std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestS
             if (rd.capacity() > dcap) {
                 check(cudaStreamSynchronize(st), "sync");
                 for (auto& p : dbytes) {
-                    cudaFree(p);
-                    check(cudaMalloc(&p, rd.capacity() + 16), "cudaMalloc");
+                    dfree(p);
+                    dalloc(&p, rd.capacity() + 16);
                 }
                 dcap = rd.capacity();
             }
@@ -552,10 +564,10 @@ std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestS
                 if (pool_bound + n > pool_cap) {
                     const uint64_t ncap = std::max<uint64_t>(2 * pool_cap, pool_bound + n + (16u << 20));
                     char* np = nullptr;
-                    check(cudaMalloc(&np, ncap), "cudaMalloc");
+                    dalloc(&np, ncap);
                     if (pool_bound) check(cudaMemcpyAsync(np, pool, pool_bound, cudaMemcpyDeviceToDevice, st), "D2D");
                     check(cudaStreamSynchronize(st), "sync");
-                    cudaFree(pool);
+                    dfree(pool);
                     pool = np;
                     pool_cap = ncap;
                 }
@@ -585,7 +597,7 @@ std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestS
         std::vector<CountedWord> out;
         if (distinct) {
             CountEntry* ent = nullptr;
-            check(cudaMalloc(&ent, distinct * sizeof(CountEntry)), "cudaMalloc");
+            dalloc(&ent, distinct * sizeof(CountEntry));
             check(cudaMemsetAsync(scalars + 3, 0, 8, st), "memset");
             table_export_kernel<<<grid_of(tab.cap), 256, 0, st>>>(tab.t, ent, scalars + 3);
             std::vector<CountEntry> host(distinct);
@@ -593,7 +605,7 @@ std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestS
             check(cudaMemcpyAsync(host.data(), ent, distinct * sizeof(CountEntry), cudaMemcpyDeviceToHost, st), "D2H");
             if (sc[0]) check(cudaMemcpyAsync(hpool.data(), pool, sc[0], cudaMemcpyDeviceToHost, st), "D2H");
             check(cudaStreamSynchronize(st), "sync");
-            cudaFree(ent);
+            dfree(ent);
             out.resize(distinct);
             for (uint64_t i = 0; i < distinct; ++i) {
                 out[i].count = static_cast<int64_t>(host[i].count);
