@@ -307,13 +307,23 @@ def main():
         record["on"] = rec
         trainer.run_pass(epoch, T, tokens_before=0)
 
+    # The clock sampler starts with the warm-up: nvidia-smi needs ~0.2 s to report its
+    # first sample, longer than a whole timed region of the small configs. Extra untimed
+    # warm-up steps run until it has reported at least once (bounded), so the reported
+    # clocks are those of the loaded GPU from the warm-up through the timed region.
+    clocks = ClockSampler(local)
+    clocks.start()
     for w in range(args.warmup):
         one_step(10_000 + w, False)
     torch.cuda.synchronize()
+    t_wait = time.perf_counter()
+    extra = 0
+    while clocks.proc is not None and not clocks.rows and time.perf_counter() - t_wait < 5.0:
+        one_step(20_000 + extra, False)
+        torch.cuda.synchronize()
+        extra += 1
     if world > 1:
         dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
     torch.cuda.synchronize()
     step_ms = []
     for s in range(args.steps):
@@ -328,6 +338,7 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    clk["window"] = "from the warm-up through the timed region (GPU under load throughout)"
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)

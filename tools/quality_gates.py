@@ -32,17 +32,15 @@ from paper_1606_07822_b200.corpus_gen import CONFIGS, cluster_raw_ids, vocab_fro
 
 
 def recall_at_10(syn0: np.ndarray, cluster: np.ndarray, sample: np.ndarray) -> float:
-    import torch
-
-    x = torch.tensor(syn0, device="cuda", dtype=torch.float32)
-    x = x / x.norm(dim=1, keepdim=True).clamp_min(1e-12)
+    """Share of the 10 exact cosine nearest neighbours (self excluded, ties to the lower
+    id) that share the query's planted cluster -- through the product's own evaluation
+    kernel (cg_nearest, cg_eval.cu), for the GPU model and the reference model alike."""
+    emb = api.Embeddings(syn0)
     hits = 0
-    for a in range(0, len(sample), 2048):
-        q = torch.tensor(sample[a:a + 2048], device="cuda")
-        sim = x[q] @ x.T
-        sim[torch.arange(len(q), device="cuda"), q] = -2.0
-        top = sim.topk(10, dim=1).indices.cpu().numpy()
-        hits += int((cluster[top] == cluster[sample[a:a + 2048]][:, None]).sum())
+    for a in range(0, len(sample), 8192):
+        q = np.ascontiguousarray(sample[a:a + 8192], dtype=np.int32)
+        ids, _ = emb.nearest(q, 10)
+        hits += int((cluster[ids] == cluster[q][:, None]).sum())
     return hits / (10 * len(sample))
 
 
