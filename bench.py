@@ -262,9 +262,16 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # One process per GPU. CG_BENCH_BACKEND=gloo (tests only) runs the N > 1 code path
+    # with every rank on the visible GPUs round-robin; timings of such a run mean nothing.
+    backend = os.environ.get("CG_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1606_07822_b200 import api
 
     c, vocab, ids = workload(args.config, rank, world, device=args.config in ("c4", "c5"))

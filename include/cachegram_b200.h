@@ -212,7 +212,7 @@ typedef struct cg_tuning {
     int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
     float hot_flush_scale;    /* 0 = per-row 1/E[#CTAs contributing per flush] (averaging of overlapping
                                  CTA replicas); > 0 = this multiplier for every cached row */
-    int32_t flush_centers;    /* 0 = 64: centers merged into a CTA's cache between flushes */
+    int32_t flush_centers;    /* 0 = 128: centers merged into a CTA's cache between flushes */
     int32_t min_cache_rows;   /* 0 = default (at least the top 31 rows are cached); < 0 = honour K exactly,
                                  even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip

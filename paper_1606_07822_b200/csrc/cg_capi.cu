@@ -703,7 +703,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.counters = s->counters.p;
             h.cold_store = s->tune.cold_update;
             const int32_t want_rows = s->tune.min_cache_rows < 0 ? s->K : s->cached_rows;
-            h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 64;
+            h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 128;  // 32: +22% K1 time at C2, 64: +8%, 256: same as 128 (profiles/r1_perf4_c2.jsonl)
             h.dummy_row = s->V - 1;
             h.probe = s->tune.probe;
             const cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,

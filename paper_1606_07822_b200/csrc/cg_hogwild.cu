@@ -393,12 +393,12 @@ __device__ __forceinline__ float chunk_signal(const float4* V, int d4, int lane,
 #pragma unroll
     for (int ii = 0; ii < CIc; ++ii) {
         const int i = min(cc + ii, nb - 1);
+        // Lanes past the row end read the neighbouring (finite: the region is zeroed at
+        // launch and only ever holds model values) shared-memory data; their U chunk is 0,
+        // so they add exact zeros to the reduction. No per-element selects.
         float4 v[DCH];
 #pragma unroll
-        for (int k = 0; k < DCH; ++k) {
-            const int q = lane + 32 * k;
-            v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
-        }
+        for (int k = 0; k < DCH; ++k) v[k] = V[i * d4 + lane + 32 * k];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             float acc = 0.f;
@@ -444,6 +444,10 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
     for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
+    {  // context, h and prefetch buffers: zeroed once so out-of-row reads are finite
+        const int n4 = ((blockDim.x >> 5) - 1) * (2 * NB + 4) * d4;  // exactly the ctx + prefetch allocation
+        for (int i = tid; i < n4; i += blockDim.x) ctx_all[i] = f4(0.f);
+    }
     if (tid == 0) {
         s_done = 0;
         s_merged = 0;
@@ -609,16 +613,18 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                             ls = 5 - Log2<2 * G>::v;
                             cic = 2;
                         }
-                        // rolled on purpose: unrolled, the kernel's hot loop outgrows the
-                        // instruction cache (ncu: 21% no_instruction stalls)
+                        // Rolled: unrolled (fully or 2x), the kernel's hot loop
+                        // outgrows the instruction cache or the registers (ncu: 21%
+                        // no_instruction stalls fully unrolled; 2x: +11% K1 time at D 300).
+                        // Lanes past the row end compute on neighbouring data; their hacc
+                        // and delta chunks are never written back.
 #pragma unroll 1
                         for (int ii = 0; ii < min(cic, r); ++ii) {
                             const int i = cc + ii;
                             float4 v[DCH], hacc[DCH];
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
-                                const int q = lane + 32 * k;
-                                v[k] = q < d4 ? V[i * d4 + q] : f4(0.f);
+                                v[k] = V[i * d4 + lane + 32 * k];
                                 hacc[k] = f4(0.f);
                             }
 #pragma unroll

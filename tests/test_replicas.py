@@ -111,3 +111,29 @@ def test_two_replicas_gloo_average_matches_sequential_simulation():
             for r in range(world):
                 models[r][:] = avg
     np.testing.assert_allclose(m0, models[0], rtol=0, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_functional(tmp_path):
+    """bench.py's N > 1 path end to end (sessions, shards, averaging through the device
+    model buffer, max-over-ranks timing, one JSON line from rank 0) with 2 ranks on the
+    one available GPU over gloo. Functional only: the ranks share the GPU."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    port = _free_port()
+    env = dict(os.environ, CG_BENCH_BACKEND="gloo", MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(root / "bench.py"), "--gpus", "2",
+           "--config", "c1", "--steps", "2", "--warmup", "1", "--no-cpu-baseline", "--e2e-steps", "1",
+           "--sync-words", "200000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(root), env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "replicas2"
+    assert d["e2e"]["value"] > 0

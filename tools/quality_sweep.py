@@ -64,6 +64,8 @@ def main():
                       dict(k=0, probe=1), dict(cold=1)]
     grids["probe34"] = [dict(kernel=kn, probe=pb) for kn in (4, 3) for pb in (0, 1, 2, 4, 7)] + \
         [dict(kernel=4, cpw=1), dict(kernel=4, cpw=16), dict(kernel=4, warps=8), dict(kernel=4, k=0)]
+    grids["perf4"] = [dict(), dict(cpw=8), dict(cpw=16), dict(flush=32), dict(flush=128), dict(flush=256),
+                      dict(warps=9), dict(warps=11), dict(cpw=16, flush=128)]
     grids["perf"] = [dict(), dict(cpw=1), dict(cpw=8), dict(cpw=16), dict(flush=16), dict(flush=256), dict(k=0),
                      dict(warps=8), dict(scale=1 / 16), dict(cold=1)]
     grids["default"] = [
