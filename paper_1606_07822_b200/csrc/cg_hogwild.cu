@@ -621,11 +621,13 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll 1
                         for (int ii = 0; ii < min(cic, r); ++ii) {
                             const int i = cc + ii;
+                            // h accumulates in place: load Hs[i] up front (with v) so the
+                            // loads overlap and the FMAs add straight into it
                             float4 v[DCH], hacc[DCH];
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 v[k] = V[i * d4 + lane + 32 * k];
-                                hacc[k] = f4(0.f);
+                                hacc[k] = Hs[i * d4 + lane + 32 * k];
                             }
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
@@ -639,7 +641,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
-                                if (q < d4) Hs[i * d4 + q] = add4(Hs[i * d4 + q], hacc[k]);
+                                if (q < d4) Hs[i * d4 + q] = hacc[k];
                             }
                         }
                         cc += cic;
