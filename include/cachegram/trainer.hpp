@@ -48,6 +48,10 @@ struct TrainConfig {
     std::int32_t flush_interval = 10;
     std::uint64_t seed = 1;
     TrainMode mode = TrainMode::Auto;
+    // B200 additions: model replicas on GPUs 0..gpus-1 of this process, averaged over
+    // peer memory every sync_words words per replica (Hogwild mode).
+    std::int32_t gpus = 1;
+    std::int64_t sync_words = 1000000;
 
     TrainMode resolved_mode() const {
         if (mode != TrainMode::Auto) return mode;
@@ -67,6 +71,8 @@ struct TrainConfig {
         need(workers >= 1, "workers must be >= 1");
         need(cache_nodes >= 0, "cache-nodes must be >= 0");
         need(flush_interval >= 1, "flush-interval must be >= 1");
+        need(gpus >= 1 && gpus <= 8, "gpus must be in [1, 8]");
+        need(sync_words >= 1, "sync-words must be >= 1");
     }
 };
 
@@ -266,8 +272,18 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
 
     Model model(vocab.size(), config.dim);
     cg_train_stats st{};
-    trainer_detail::check(cg_train_file(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(), words.data(),
-                                        model.input_matrix().data(), model.weight_matrix().data(), &st));
+    if (config.gpus > 1) {
+        if (mode != TrainMode::Hogwild) throw std::invalid_argument("gpus > 1 trains replicas in Hogwild mode");
+        std::vector<std::int32_t> devices(static_cast<std::size_t>(config.gpus));
+        for (std::int32_t g = 0; g < config.gpus; ++g) devices[static_cast<std::size_t>(g)] = g;
+        trainer_detail::check(cg_train_file_replicas(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(),
+                                                     words.data(), devices.data(), config.gpus, config.sync_words,
+                                                     model.input_matrix().data(), model.weight_matrix().data(), &st));
+    } else {
+        trainer_detail::check(cg_train_file(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(),
+                                            words.data(), model.input_matrix().data(),
+                                            model.weight_matrix().data(), &st));
+    }
     if (stats) {
         stats->words_processed = st.words_processed;
         stats->wall_seconds = st.wall_seconds;

@@ -239,6 +239,24 @@ CG_API int cg_session_load_corpus(cg_session* s, const char* path, const char* w
 CG_API int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const char* corpus_path,
                          const char* words_nul, float* syn0_out, float* syn1_out, cg_train_stats* stats);
 
+/* ---- in-process replicas: one model replica per GPU -------------------
+ * For C/C++ callers that drive several GPUs from one process. Each replica trains a
+ * contiguous shard of the id stream (Hogwild mode); every sync_words words per replica
+ * the replicas are averaged over peer memory (NVLink/NVSwitch): replica r's GPU averages
+ * slice r across all replicas and writes it back to all of them. The learning rate
+ * follows n_devices x local progress. devices may repeat an ordinal (several replicas
+ * on one GPU: functional testing). The result is replica 0's model (all are equal). */
+CG_API int cg_train_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids,
+                             int64_t n_ids, const int32_t* devices, int32_t n_devices, int64_t sync_words,
+                             float* syn0_out, float* syn1_out, cg_train_stats* stats);
+/* Same with the corpus as a file, tokenised on devices[0] and sharded device to device. */
+CG_API int cg_train_file_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model,
+                                  const char* corpus_path, const char* words_nul, const int32_t* devices,
+                                  int32_t n_devices, int64_t sync_words, float* syn0_out, float* syn1_out,
+                                  cg_train_stats* stats);
+/* In-place average of n (<= 8) equally sized device buffers over peer memory. */
+CG_API int cg_average_buffers(void* const* device_bufs, const int32_t* devices, int32_t n, size_t n_floats);
+
 /* ---- evaluation (eval.hpp:88-238) ---------------------------
  * A device-resident table of unit-normalised rows, built exactly like AnalogySolver
  * (eval.hpp:91-103): row / sqrtf(dot(row, row)), zeros when the norm is not > 0.

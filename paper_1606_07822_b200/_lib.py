@@ -145,6 +145,12 @@ SIGNATURES = {
     "cg_session_load_corpus": (C.c_int, [vp, C.c_char_p, C.c_char_p, P(C.c_int64)]),
     "cg_train_file": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), C.c_char_p, C.c_char_p, P(C.c_float),
                                 P(C.c_float), P(CgTrainStats)]),
+    "cg_train_replicas": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), P(C.c_int32), C.c_int64, P(C.c_int32),
+                                    C.c_int32, C.c_int64, P(C.c_float), P(C.c_float), P(CgTrainStats)]),
+    "cg_train_file_replicas": (C.c_int, [P(CgConfig), C.c_int32, P(CgModelDesc), C.c_char_p, C.c_char_p,
+                                         P(C.c_int32), C.c_int32, C.c_int64, P(C.c_float), P(C.c_float),
+                                         P(CgTrainStats)]),
+    "cg_average_buffers": (C.c_int, [P(vp), P(C.c_int32), C.c_int32, C.c_size_t]),
     "cg_embeddings_create": (C.c_int, [P(C.c_float), C.c_int32, C.c_int32, C.c_int32, P(vp)]),
     "cg_embeddings_create_device": (C.c_int, [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, P(vp)]),
     "cg_embeddings_destroy": (None, [vp]),

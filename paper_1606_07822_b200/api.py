@@ -108,7 +108,10 @@ class Vocabulary:
 
     def __del__(self):
         if getattr(self, "_handle", None):
-            load().cg_corpus_close(self._handle)
+            try:
+                load().cg_corpus_close(self._handle)
+            except Exception:  # interpreter teardown: the library may already be gone
+                pass
             self._handle = None
 
 
@@ -390,11 +393,13 @@ def train_center(center: int, sentence: Sequence[int], center_pos: int, half_win
 
 # --------------------------------------------------------------------------- train()
 def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelection, config: TrainConfig,
-          stats: TrainStats | None = None) -> Model:
+          stats: TrainStats | None = None, devices: Sequence[int] | None = None,
+          sync_words: int = 1_000_000) -> Model:
     """cachegram::train (trainer.hpp:254-316) on the GPU.
 
-    ``corpus`` is a corpus file path (read with the library's tokenizer) or an
-    in-vocabulary int32 id stream."""
+    ``corpus`` is a corpus file path (tokenised on the GPU) or an in-vocabulary int32 id
+    stream. ``devices`` (Hogwild mode) trains one model replica per listed GPU of this
+    process, averaged over peer memory every ``sync_words`` words per replica."""
     config.validate()
     _check_consistency(vocab, tree, selection)
     mode = resolve_mode(config)
@@ -405,15 +410,26 @@ def train(corpus, vocab: Vocabulary, tree: HuffmanTree, selection: CacheSelectio
     cfg = config.to_c()
     m = Model(vocab.size(), config.dim)
     st = CgTrainStats()
-    if isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__"):
-        # tokenised on the GPU, like the drop-in C++ train(corpus_path, ...)
-        words = b"".join(vocab.word(w).encode("utf-8", "surrogateescape") + b"\0" for w in range(vocab.size()))
-        check(load().cg_train_file(C.byref(cfg), MODES[mode], C.byref(desc), str(corpus).encode(), words,
-                                   ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
+    is_file = isinstance(corpus, (str, bytes)) or hasattr(corpus, "__fspath__")
+    words = b"".join(vocab.word(w).encode("utf-8", "surrogateescape") + b"\0" for w in range(vocab.size())) \
+        if is_file else b""
+    ids = None if is_file else np.ascontiguousarray(np.asarray(corpus, np.int32))
+    out0, out1 = ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float)
+    if devices is not None:
+        dev = np.ascontiguousarray(np.asarray(devices, np.int32))
+        if is_file:  # tokenised on devices[0], sharded device to device
+            check(load().cg_train_file_replicas(C.byref(cfg), MODES[mode], C.byref(desc), str(corpus).encode(), words,
+                                                ptr(dev, C.c_int32), dev.size, int(sync_words), out0, out1,
+                                                C.byref(st)))
+        else:
+            check(load().cg_train_replicas(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
+                                           ptr(dev, C.c_int32), dev.size, int(sync_words), out0, out1, C.byref(st)))
+    elif is_file:  # tokenised on the GPU, like the drop-in C++ train(corpus_path, ...)
+        check(load().cg_train_file(C.byref(cfg), MODES[mode], C.byref(desc), str(corpus).encode(), words, out0, out1,
+                                   C.byref(st)))
     else:
-        ids = np.ascontiguousarray(np.asarray(corpus, np.int32))
-        check(load().cg_train(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size,
-                              ptr(m.syn0, C.c_float), ptr(m.syn1, C.c_float), C.byref(st)))
+        check(load().cg_train(C.byref(cfg), MODES[mode], C.byref(desc), ptr(ids, C.c_int32), ids.size, out0, out1,
+                              C.byref(st)))
     if stats is not None:
         stats.words_processed = st.words_processed
         stats.wall_seconds = st.wall_seconds
@@ -448,7 +464,10 @@ class Session:
             self._h = C.c_void_p()
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter teardown
+            pass
 
     def upload_ids(self, ids: np.ndarray) -> None:
         ids = np.ascontiguousarray(ids, np.int32)
@@ -630,7 +649,10 @@ class Embeddings:
 
     def __del__(self):
         if getattr(self, "_h", None):
-            load().cg_embeddings_destroy(self._h)
+            try:
+                load().cg_embeddings_destroy(self._h)
+            except Exception:  # interpreter teardown
+                pass
             self._h = None
 
 

@@ -10,7 +10,10 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
+#include <barrier>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -1268,6 +1271,257 @@ int cg_corpus_read_ids_gpu(const cg_corpus* c, const char* path, int32_t device,
         }
         CG_CUDA(cudaStreamSynchronize(st));
         cudaStreamDestroy(st);
+    });
+}
+
+}  // extern "C"
+
+// ============================================================================ in-process replicas
+// One model replica per GPU of this process, for C/C++ callers that do not
+// run one process per GPU: each replica trains its shard of the id stream, and every
+// `sync_words` words per replica the replicas are averaged in place over peer memory
+// (NVLink/NVSwitch): replica r's device averages slice r of the model buffer across all
+// replicas and writes the mean back to every replica -- a reduce-scatter and an
+// all-gather in one pass, the same bytes per GPU as a ring all-reduce.
+namespace {
+constexpr int kMaxReplicas = 8;
+struct ReplicaPtrs {
+    float4* buf[kMaxReplicas];
+};
+
+__global__ void replica_avg_kernel(ReplicaPtrs p, int n, size_t begin4, size_t end4, float inv_n) {
+    for (size_t i = begin4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < end4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        float4 s = p.buf[0][i];
+        for (int r = 1; r < n; ++r) {  // fixed order: every replica receives the same bits
+            const float4 x = p.buf[r][i];
+            s.x += x.x;
+            s.y += x.y;
+            s.z += x.z;
+            s.w += x.w;
+        }
+        s = make_float4(s.x * inv_n, s.y * inv_n, s.z * inv_n, s.w * inv_n);
+        for (int r = 0; r < n; ++r) p.buf[r][i] = s;
+    }
+}
+
+void enable_peers(const int32_t* devices, int32_t n) {
+    for (int32_t a = 0; a < n; ++a)
+        for (int32_t b = 0; b < n; ++b) {
+            if (devices[a] == devices[b]) continue;
+            int ok = 0;
+            CG_CUDA(cudaDeviceCanAccessPeer(&ok, devices[a], devices[b]));
+            if (!ok) throw CgError(CG_ERR_CUDA, "replica devices cannot access each other's memory (no P2P)");
+            CG_CUDA(cudaSetDevice(devices[a]));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CG_CUDA(e);
+            cudaGetLastError();
+        }
+}
+
+// Replica r's share of the averaging: slice r of n4 float4s, launched on devices[r].
+void launch_average_slice(const ReplicaPtrs& p, int32_t n, int32_t r, size_t n4, int32_t device, cudaStream_t st) {
+    const size_t b = n4 * static_cast<size_t>(r) / static_cast<size_t>(n);
+    const size_t e = n4 * static_cast<size_t>(r + 1) / static_cast<size_t>(n);
+    if (e <= b) return;
+    CG_CUDA(cudaSetDevice(device));
+    const unsigned grid = static_cast<unsigned>(std::min<size_t>((e - b + 255) / 256, 148 * 8));
+    replica_avg_kernel<<<grid, 256, 0, st>>>(p, n, b, e, 1.0f / static_cast<float>(n));
+    CG_CUDA(cudaGetLastError());
+}
+
+void check_replica_devices(const int32_t* devices, int32_t n) {
+    if (n < 1 || n > kMaxReplicas) invalid("replica count must be in [1, 8]");
+    if (!devices) invalid("null device list");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        throw CgError(CG_ERR_CUDA, "no CUDA device available (the GPU path has no CPU fallback)");
+    }
+    for (int32_t r = 0; r < n; ++r)
+        if (devices[r] < 0 || devices[r] >= ndev) invalid("device ordinal out of range");
+}
+
+// The shared driver of cg_train_replicas / cg_train_file_replicas. `load(r, s)` fills
+// replica r's session with its shard and returns the shard length.
+template <typename Load>
+void run_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* devices, int32_t n,
+                  int64_t sync_words, Load&& load, float* syn0_out, float* syn1_out, cg_train_stats* stats) {
+    if (!cfg || !model) invalid("null config or model");
+    if (mode != CG_MODE_HOGWILD) invalid("replicas train in Hogwild mode (the deterministic mode is one stream)");
+    if (sync_words < 1) invalid("sync_words must be >= 1");
+    check_replica_devices(devices, n);
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Rep {
+        cg_session* s = nullptr;
+        cudaStream_t st = nullptr;
+        int64_t len = 0;
+        double kernel_s = 0.0;
+        uint64_t centers = 0, pairs = 0, steps = 0, words = 0;
+    };
+    std::vector<Rep> rep(static_cast<size_t>(n));
+    auto cleanup = [&] {
+        for (auto& x : rep) {
+            if (x.s) cg_session_destroy(x.s);
+            if (x.st) cudaStreamDestroy(x.st);
+        }
+    };
+    try {
+        for (int32_t r = 0; r < n; ++r) {
+            Rep& x = rep[static_cast<size_t>(r)];
+            CG_CUDA(cudaSetDevice(devices[r]));
+            CG_CUDA(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
+            const int rc = cg_session_create(cfg, mode, model, devices[r], x.st, &x.s);
+            if (rc != CG_OK) throw CgError(rc, g_error);
+            x.len = load(r, x.s);
+        }
+        enable_peers(devices, n);
+        ReplicaPtrs ptrs{};
+        size_t bytes = 0;
+        for (int32_t r = 0; r < n; ++r) {
+            void* p = nullptr;
+            int32_t stride = 0;
+            const int rc = cg_session_model_buffer(rep[static_cast<size_t>(r)].s, &p, &bytes, &stride);
+            if (rc != CG_OK) throw CgError(rc, g_error);
+            ptrs.buf[r] = static_cast<float4*>(p);
+        }
+        const size_t n4 = bytes / sizeof(float4);
+        int64_t max_len = 0;
+        for (auto& x : rep) max_len = std::max(max_len, x.len);
+        const int64_t chunks = (max_len + sync_words - 1) / sync_words;
+        std::barrier sync(n);
+        std::atomic<int> failed{0};
+        std::vector<std::string> errs(static_cast<size_t>(n));
+        std::vector<int> codes(static_cast<size_t>(n), CG_OK);
+        auto worker = [&](int32_t r) {
+            Rep& x = rep[static_cast<size_t>(r)];
+            for (int32_t it = 0; it < cfg->iterations; ++it) {
+                for (int64_t c = 0; c < chunks; ++c) {
+                    if (!failed.load()) {
+                        const int64_t a = std::min(x.len, c * sync_words), b = std::min(x.len, (c + 1) * sync_words);
+                        cg_epoch_stats e{};
+                        const uint64_t base = (static_cast<uint64_t>(it) * static_cast<uint64_t>(x.len) + static_cast<uint64_t>(a)) *
+                                              static_cast<uint64_t>(n);
+                        const int rc = b > a ? cg_session_train_range(x.s, it, a, b, base, static_cast<uint32_t>(n), &e)
+                                             : CG_OK;
+                        if (rc != CG_OK) {
+                            codes[static_cast<size_t>(r)] = rc;
+                            errs[static_cast<size_t>(r)] = cg_last_error();
+                            failed.store(1);
+                        }
+                        x.kernel_s += (e.train_ms + e.subsample_ms) * 1e-3;
+                        x.centers += e.kept;
+                        x.pairs += e.pairs;
+                        x.steps += e.steps;
+                        x.words += e.words;
+                    }
+                    sync.arrive_and_wait();  // every replica finished this chunk
+                    if (!failed.load() && n > 1) {
+                        try {
+                            launch_average_slice(ptrs, n, r, n4, devices[r], x.st);
+                            CG_CUDA(cudaStreamSynchronize(x.st));
+                        } catch (const std::exception& ex) {
+                            codes[static_cast<size_t>(r)] = CG_ERR_CUDA;
+                            errs[static_cast<size_t>(r)] = ex.what();
+                            failed.store(1);
+                        }
+                    }
+                    sync.arrive_and_wait();  // every slice averaged
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int32_t r = 1; r < n; ++r) pool.emplace_back(worker, r);
+        worker(0);
+        for (auto& t : pool) t.join();
+        for (int32_t r = 0; r < n; ++r)
+            if (codes[static_cast<size_t>(r)] != CG_OK)
+                throw CgError(codes[static_cast<size_t>(r)], "replica " + std::to_string(r) + " failed: " + errs[static_cast<size_t>(r)]);
+        const int rc = cg_session_download(rep[0].s, syn0_out, syn1_out);
+        if (rc != CG_OK) throw CgError(rc, g_error);
+        cg_train_stats out{};
+        for (auto& x : rep) {
+            out.words_processed += x.words;
+            out.centers += x.centers;
+            out.pairs += x.pairs;
+            out.steps += x.steps;
+            out.kernel_seconds = std::max(out.kernel_seconds, x.kernel_s);
+        }
+        out.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        out.words_per_second = out.wall_seconds > 0 ? static_cast<double>(out.words_processed) / out.wall_seconds : 0.0;
+        if (stats) *stats = out;
+    } catch (...) {
+        cleanup();
+        throw;
+    }
+    cleanup();
+}
+}  // namespace
+
+extern "C" {
+
+int cg_average_buffers(void* const* device_bufs, const int32_t* devices, int32_t n, size_t n_floats) {
+    return guarded([&] {
+        if (!device_bufs) invalid("null buffer list");
+        check_replica_devices(devices, n);
+        if (n_floats % 4) invalid("n_floats must be a multiple of 4");
+        enable_peers(devices, n);
+        ReplicaPtrs p{};
+        for (int32_t r = 0; r < n; ++r) p.buf[r] = static_cast<float4*>(device_bufs[r]);
+        for (int32_t r = 0; r < n; ++r) launch_average_slice(p, n, r, n_floats / 4, devices[r], nullptr);
+        for (int32_t r = 0; r < n; ++r) {
+            CG_CUDA(cudaSetDevice(devices[r]));
+            CG_CUDA(cudaDeviceSynchronize());
+        }
+    });
+}
+
+int cg_train_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids, int64_t n_ids,
+                      const int32_t* devices, int32_t n_devices, int64_t sync_words, float* syn0_out, float* syn1_out,
+                      cg_train_stats* stats) {
+    return guarded([&] {
+        if (n_ids < 0 || (n_ids > 0 && !ids)) invalid("bad id stream");
+        run_replicas(cfg, mode, model, devices, n_devices, sync_words,
+                     [&](int32_t r, cg_session* s) -> int64_t {
+                         // contiguous near-equal shards (corpus.hpp:192-223 on the id stream)
+                         const int64_t a = n_ids * r / n_devices, b = n_ids * (r + 1) / n_devices;
+                         const int rc = cg_session_upload_ids(s, ids + a, b - a);
+                         if (rc != CG_OK) throw CgError(rc, g_error);
+                         return b - a;
+                     },
+                     syn0_out, syn1_out, stats);
+    });
+}
+
+int cg_train_file_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const char* corpus_path,
+                           const char* words_nul, const int32_t* devices, int32_t n_devices, int64_t sync_words,
+                           float* syn0_out, float* syn1_out, cg_train_stats* stats) {
+    return guarded([&] {
+        if (!corpus_path || !words_nul || !model) invalid("null argument");
+        check_replica_devices(devices, n_devices);
+        // tokenise once on the first replica's GPU, then hand each replica its shard
+        CG_CUDA(cudaSetDevice(devices[0]));
+        const std::vector<std::string> words = split_nul(words_nul, model->vocab_size);
+        DevBuf<int32_t> all;
+        cudaStream_t st = nullptr;
+        CG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        int64_t n_ids = 0;
+        try {
+            n_ids = device_id_stream(corpus_path, words, model->total_tokens, all, st, nullptr);
+            CG_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        cudaStreamDestroy(st);
+        run_replicas(cfg, mode, model, devices, n_devices, sync_words,
+                     [&](int32_t r, cg_session* s) -> int64_t {
+                         const int64_t a = n_ids * r / n_devices, b = n_ids * (r + 1) / n_devices;
+                         const int rc = cg_session_upload_ids_device(s, all.p + a, b - a);
+                         if (rc != CG_OK) throw CgError(rc, g_error);
+                         return b - a;
+                     },
+                     syn0_out, syn1_out, stats);
     });
 }
 

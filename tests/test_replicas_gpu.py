@@ -1,0 +1,81 @@
+"""In-process replicas (cg_train_replicas / cg_train_file_replicas / cg_average_buffers):
+the peer-memory averaging kernel is exact (fixed summation order, identical bits on every
+replica), and replicated training covers every token once per pass with the quality of
+a single replica. The box has one GPU, so the replicas share device 0 -- the same code
+paths, with peer pointers that happen to be local."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import fixtures as F
+import oracle_lib as O
+from paper_1606_07822_b200 import _lib, api
+
+pytestmark = pytest.mark.gpu
+
+
+def test_average_buffers_exact():
+    import torch
+
+    rng = np.random.default_rng(3)
+    host = [rng.standard_normal(4096 * 3 + 4).astype(np.float32) for _ in range(3)]
+    bufs = [torch.from_numpy(h).cuda() for h in host]
+    ptrs = (C.c_void_p * 3)(*[b.data_ptr() for b in bufs])
+    dev = np.zeros(3, np.int32)
+    _lib.check(_lib.load().cg_average_buffers(ptrs, _lib.ptr(dev, C.c_int32), 3, host[0].size))
+    want = ((host[0] + host[1]) + host[2]) * np.float32(1.0 / 3.0)
+    for b in bufs:
+        assert np.array_equal(b.cpu().numpy().view(np.uint32), want.view(np.uint32))
+    with pytest.raises(ValueError):
+        _lib.check(_lib.load().cg_average_buffers(ptrs, _lib.ptr(dev, C.c_int32), 3, 5))
+
+
+def _setup(tmp_path):
+    path = F.write(tmp_path / "r.txt", F.make_zipf_corpus(600_000, 3000, 5))
+    vocab = api.build_vocabulary_file(path, 2)
+    ids = api.read_id_stream(path, vocab)
+    tree = api.build_huffman_tree(vocab)
+    sel = api.select_cached_nodes(tree, 31)
+    return path, vocab, ids, tree, sel
+
+
+def _loss(m, vocab, ids, tree, cfg):
+    t = O.Tree(tree.offsets, tree.nodes, tree.turns, tree.usage)
+    cen, ctx = O.sample_pairs(ids, vocab.counts, vocab.total_tokens(), cfg["sample"], cfg["window"], 99, 1 << 16)
+    return O.hs_loss(cen, ctx, m.syn0, m.syn1, t)
+
+
+@pytest.mark.parametrize("n_rep", [1, 2, 3])
+def test_replicas_cover_the_stream_and_learn(tmp_path, n_rep):
+    """Weak scaling, as in bench.py at N GPUs: every replica trains a full-size shard (here
+    n_rep copies of the corpus), so the averaged model must learn as much as one replica
+    on one copy. (With a fixed corpus split n ways, model averaging learns roughly 1/n as
+    much per pass -- the known cost of synchronous averaging.)"""
+    path, vocab, ids, tree, sel = _setup(tmp_path)
+    cfg = dict(dim=32, window=5, min_count=2, sample=1e-3, iterations=2, cache_nodes=31, seed=4)
+    tc = api.TrainConfig(**cfg, mode="hogwild")
+    single = api.train(ids, vocab, tree, sel, tc)
+    st = api.TrainStats()
+    stream = np.tile(ids, n_rep)
+    vocab_n = api.Vocabulary(vocab.counts * n_rep, vocab.words)  # totals of the n-copy stream
+    rep = api.train(stream, vocab_n, tree, sel, tc, st, devices=[0] * n_rep, sync_words=20_000)
+    assert st.words_processed == stream.size * 2
+    assert np.isfinite(rep.syn0).all() and np.isfinite(rep.syn1).all()
+    init = api.init_model(vocab.size(), 32, 4)
+    l_init, l_one, l_rep = (_loss(m, vocab, ids, tree, cfg) for m in (init, single, rep))
+    assert l_one < l_init and l_rep < l_init
+    assert (l_init - l_rep) > 0.8 * (l_init - l_one), (l_init, l_one, l_rep)
+
+
+def test_file_replicas_match_id_replicas_in_coverage(tmp_path):
+    path, vocab, ids, tree, sel = _setup(tmp_path)
+    tc = api.TrainConfig(dim=16, window=3, min_count=2, sample=1e-3, iterations=1, cache_nodes=31, seed=9,
+                         mode="hogwild")
+    st = api.TrainStats()
+    m = api.train(path, vocab, tree, sel, tc, st, devices=[0, 0], sync_words=50_000)
+    assert st.words_processed == ids.size
+    assert np.isfinite(m.syn0).all()
+    with pytest.raises(ValueError):  # deterministic replicas are refused
+        api.train(ids, vocab, tree, sel, api.TrainConfig(dim=16, window=3, min_count=2, iterations=1,
+                                                          mode="deterministic", workers=1), devices=[0, 0])
