@@ -445,7 +445,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
     for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
     {  // context, h and prefetch buffers: zeroed once so out-of-row reads are finite
-        const int n4 = ((blockDim.x >> 5) - 1) * (2 * NB + 4) * d4;  // exactly the ctx + prefetch allocation
+        const int n4 = ((blockDim.x >> 5) - 1) * (2 * NB + G) * d4;  // exactly the ctx + prefetch allocation
         for (int i = tid; i < n4; i += blockDim.x) ctx_all[i] = f4(0.f);
     }
     if (tid == 0) {
@@ -598,20 +598,23 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                         // chunk of 8, 4 or 2 contexts: a center's 2b contexts (b = 1..W) are
                         // covered without computing dots for padding (a fixed 8 wasted ~40%)
                         const int r = nb - cc;
+                        constexpr int CIM = 32 / G;  // contexts per full chunk (CIM * G = 32 dots)
                         float gl;
                         int ls, cic;
-                        if (r >= 8) {
-                            gl = chunk_signal<DCH, G, 8>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
-                            ls = 5 - Log2<8 * G>::v;
-                            cic = 8;
-                        } else if (r >= 4) {
-                            gl = chunk_signal<DCH, G, 4>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
-                            ls = 5 - Log2<4 * G>::v;
-                            cic = 4;
+                        if (r >= CIM) {
+                            gl = chunk_signal<DCH, G, CIM>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
+                            ls = 5 - Log2<CIM * G>::v;
+                            cic = CIM;
+                        } else if (r >= CIM / 2) {
+                            gl = chunk_signal<DCH, G, CIM / 2>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale,
+                                                               alpha);
+                            ls = 5 - Log2<CIM / 2 * G>::v;
+                            cic = CIM / 2;
                         } else {
-                            gl = chunk_signal<DCH, G, 2>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
-                            ls = 5 - Log2<2 * G>::v;
-                            cic = 2;
+                            gl = chunk_signal<DCH, G, CIM / 4>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale,
+                                                               alpha);
+                            ls = 5 - Log2<CIM / 4 * G>::v;
+                            cic = CIM / 4;
                         }
                         // Rolled: unrolled (fully or 2x), the kernel's hot loop
                         // outgrows the instruction cache or the registers (ncu: 21%
@@ -702,9 +705,17 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     }
 }
 
+// v4 rows per group and worker warps per CTA. G = 8 for D <= 128 measured worse (C1 K1
+// 3.66 -> 4.48 ms): its registers only fit 11 workers -- ptxas budgets registers for a
+// multiple of 4 warps, so 13 workers would get 128 and spill.
+template <int DCH>
+constexpr int kG4 = 4;
+template <int DCH>
+constexpr int kW4 = DCH == 1 ? 15 : (DCH == 2 ? 11 : 7);
+
 template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : hog4_kernel<DCH, 4, WORKERS>;  // v4: G = 4, CI = 8
+    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>;
     if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
@@ -758,7 +769,9 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g.variant = (d4 + 31) / 32;
-    const int workers = g.variant == 1 ? Variant<1>::WORKERS : (g.variant == 2 ? Variant<2>::WORKERS : Variant<3>::WORKERS);
+    const int workers = g.kernel == 4
+                            ? (g.variant == 1 ? kW4<1> : (g.variant == 2 ? kW4<2> : kW4<3>))
+                            : (g.variant == 1 ? Variant<1>::WORKERS : (g.variant == 2 ? Variant<2>::WORKERS : Variant<3>::WORKERS));
     g.warps = warps_override > 0 ? std::min(warps_override, workers) : workers;
     g.blocks = blocks_override > 0 ? blocks_override : sms;
     g.cpw = std::min(cpw_override > 0 ? cpw_override : 4, 32);  // <= 32: a ticket's metadata is one lane each
@@ -775,7 +788,8 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     // drop up to 3 warps if that lets one batch hold a full window (2W contexts).
     const size_t budget = 225 * 1024;
     auto batch_for = [&](int warps, size_t* smem) {
-        const size_t prefetch = g.kernel == 4 ? static_cast<size_t>(warps) * 4 * d4 * 16 : 0;
+        const int g4 = g.variant == 1 ? kG4<1> : (g.variant == 2 ? kG4<2> : kG4<3>);
+        const size_t prefetch = g.kernel == 4 ? static_cast<size_t>(warps) * g4 * d4 * 16 : 0;
         const size_t per_ctx = static_cast<size_t>(warps) * 2 * d4 * 16;
         const size_t room = budget > fixed + cache_bytes + prefetch ? budget - fixed - cache_bytes - prefetch : 0;
         int nb = static_cast<int>(std::min<size_t>(2 * static_cast<size_t>(window), room / per_ctx));
