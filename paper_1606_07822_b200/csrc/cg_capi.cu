@@ -7,6 +7,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -791,14 +793,23 @@ int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, con
         cudaGetLastError();
         dev = 0;
     }
+    const auto tc = std::chrono::steady_clock::now();
     int rc = cg_session_create(cfg, mode, model, dev, nullptr, &s);
     if (rc != CG_OK) return rc;
     const auto t0 = std::chrono::steady_clock::now();
     rc = cg_session_upload_ids(s, ids, n_ids);
+    const auto t1 = std::chrono::steady_clock::now();
     cg_train_stats st{};
     if (rc == CG_OK) rc = cg_session_train(s, &st);
+    const auto t2 = std::chrono::steady_clock::now();
     if (rc == CG_OK) rc = cg_session_download(s, syn0_out, syn1_out);
-    st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const auto t3 = std::chrono::steady_clock::now();
+    st.wall_seconds = std::chrono::duration<double>(t3 - t0).count();
+    if (std::getenv("CG_PROFILE")) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "cg_train: create %.2f ms, upload %.2f ms, train %.2f ms (kernels %.2f), download %.2f ms\n",
+                     ms(tc, t0), ms(t0, t1), ms(t1, t2), st.kernel_seconds * 1e3, ms(t2, t3));
+    }
     st.words_per_second = st.wall_seconds > 0 ? static_cast<double>(st.words_processed) / st.wall_seconds : 0.0;
     if (stats) *stats = st;
     cg_session_destroy(s);
