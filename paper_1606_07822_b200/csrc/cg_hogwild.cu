@@ -635,13 +635,15 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                                 v[k] = V[i * d4 + lane + 32 * k];
                                 hacc[k] = Hs[i * d4 + lane + 32 * k];
                             }
+                            float gg[G];
+#pragma unroll
+                            for (int g = 0; g < G; ++g) gg[g] = __shfl_sync(kFull, gl, (ii * G + g) << ls);
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
-                                const float gg = __shfl_sync(kFull, gl, (ii * G + g) << ls);
 #pragma unroll
                                 for (int k = 0; k < DCH; ++k) {
-                                    hacc[k] = axpy4(gg, U[g][k], hacc[k]);
-                                    Dl[g][k] = axpy4(gg, v[k], Dl[g][k]);
+                                    hacc[k] = axpy4(gg[g], U[g][k], hacc[k]);
+                                    Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
                                 }
                             }
 #pragma unroll
