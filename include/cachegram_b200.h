@@ -216,7 +216,8 @@ typedef struct cg_tuning {
     int32_t min_cache_rows;   /* 0 = default (at least the top 31 rows are cached); < 0 = honour K exactly,
                                  even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
-                                 context-row updates, bit 2 skip cache merges */
+                                 context-row updates, bit 2 skip cache merges, bit 3 skip reading the
+                                 CTA's cached deltas */
     int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);

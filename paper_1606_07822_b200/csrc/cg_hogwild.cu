@@ -589,7 +589,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                             float4 u = f4(0.f);
                             if (q < d4) {
                                 u = Ub[g * d4 + q];
-                                if (row[g] < K) u = add4(u, dblk[row[g] * d4 + q]);  // + this CTA's cached delta
+                                if (row[g] < K && !(a.probe & 8)) u = add4(u, dblk[row[g] * d4 + q]);  // + this CTA's cached delta
                             }
                             U[g][k] = u;
                             Dl[g][k] = f4(0.f);

@@ -67,6 +67,7 @@ def main():
     grids["perf4"] = [dict(), dict(cpw=8), dict(cpw=16), dict(flush=32), dict(flush=128), dict(flush=256),
                       dict(warps=9), dict(warps=11), dict(cpw=16, flush=128)]
     grids["warps"] = [dict(), dict(warps=4), dict(warps=5), dict(warps=6), dict(k=64), dict(k=255)]
+    grids["probe8"] = [dict(), dict(probe=8), dict(probe=4), dict(probe=12)]
     grids["perf"] = [dict(), dict(cpw=1), dict(cpw=8), dict(cpw=16), dict(flush=16), dict(flush=256), dict(k=0),
                      dict(warps=8), dict(scale=1 / 16), dict(cold=1)]
     grids["default"] = [
