@@ -13,6 +13,14 @@ import oracle_lib as O
 from paper_1606_07822_b200 import _lib, api
 from paper_1606_07822_b200.corpus_gen import vocab_from_raw, zipf_raw_ids
 
+
+def _has_cuda() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
 HEADER = O.ROOT / "include" / "cachegram_b200.h"
 
 
@@ -127,3 +135,33 @@ def test_training_refuses_without_device_or_bad_args():
     else:
         assert rc == 0
         lib.cg_session_destroy(s)
+
+
+@pytest.mark.skipif(_has_cuda(), reason="checks the behaviour without a device")
+def test_gpu_entry_points_fail_loudly_without_a_device(tmp_path):
+    """No CPU fallback: every device entry point reports CG_ERR_CUDA on a host without a
+    GPU (argument errors are still reported first where they are checked first)."""
+    lib = _lib.load()
+    v = np.ones((4, 3), np.float32)
+    h = C.c_void_p()
+    assert lib.cg_embeddings_create(_lib.ptr(v, C.c_float), 4, 3, -1, C.byref(h)) == _lib.CG_ERR_CUDA
+    p = F.write(tmp_path / "c.txt", "a b a c")
+    assert lib.cg_corpus_open_gpu(str(p).encode(), 1, 0, C.byref(h)) == _lib.CG_ERR_CUDA
+    dev = np.zeros(2, np.int32)
+    st = _lib.CgTrainStats()
+    cfg = api.TrainConfig(dim=4, window=2, min_count=1, iterations=1).to_c()
+    counts = np.array([3, 2, 1], np.int64)
+    tree = api.build_huffman_tree(counts)
+    sel = api.select_cached_nodes(tree, 1)
+    keep: list = []
+    desc = api.model_desc(api.Vocabulary(counts), tree, sel, keep)
+    ids = np.array([0, 1, 2, 0], np.int32)
+    out0 = np.zeros((3, 4), np.float32)
+    out1 = np.zeros((2, 4), np.float32)
+    args = (C.byref(cfg), 1, C.byref(desc), _lib.ptr(ids, C.c_int32), 4, _lib.ptr(dev, C.c_int32), 2, 100,
+            _lib.ptr(out0, C.c_float), _lib.ptr(out1, C.c_float), C.byref(st))
+    assert lib.cg_train_replicas(*args) == _lib.CG_ERR_INVALID_ARGUMENT  # deterministic replicas
+    args = (C.byref(cfg), 0) + args[2:]
+    assert lib.cg_train_replicas(*args) == _lib.CG_ERR_CUDA
+    assert lib.cg_train(C.byref(cfg), 0, C.byref(desc), _lib.ptr(ids, C.c_int32), 4, _lib.ptr(out0, C.c_float),
+                        _lib.ptr(out1, C.c_float), C.byref(st)) == _lib.CG_ERR_CUDA
