@@ -710,9 +710,9 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     }
 }
 
-// v4 rows per group and worker warps per CTA. G = 8 for D <= 128 measured worse (C1 K1
-// 3.66 -> 4.48 ms): its registers only fit 11 workers -- ptxas budgets registers for a
-// multiple of 4 warps, so 13 workers would get 128 and spill.
+// v4 rows per group and worker warps per CTA. G = 8 measured worse: for D <= 128 (C1 K1
+// 3.66 -> 4.48 ms, 11 workers: ptxas budgets registers for a multiple of 4 warps, so 13
+// workers would get 128 and spill) and for D <= 256 (C2 90 -> 124 ms, 7 workers).
 template <int DCH>
 constexpr int kG4 = 4;
 template <int DCH>
