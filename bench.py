@@ -362,13 +362,14 @@ def main():
     per_launch_bytes = agg["bytes"] / n_launch
     per_launch_ms = agg["train_ms"] / n_launch
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    traffic = None
+    traffic = l2_traffic = None
     prof = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            tj = json.loads(prof.read_text())
+            traffic, l2_traffic = tj.get("dram_bytes_per_launch"), tj.get("l2_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic = l2_traffic = None
 
     # end to end through the public API with host buffers (pinned): ids H2D, model init,
     # subsampling + training (+ averaging at N > 1), model D2H. N = 1 goes through the
@@ -458,7 +459,7 @@ def main():
                        "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}",
                        "sync_words_per_gpu": args.sync_words if world > 1 else None},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
+                         "traffic": traffic, "l2_traffic": l2_traffic, "peak_source": peak_src,
                          "kernel": "hog_kernel (K1)", "algorithmic_bytes_per_launch": per_launch_bytes,
                          "kernel_ms_per_launch": per_launch_ms},
             "cpu_baseline": cpu,

@@ -59,11 +59,19 @@ def main():
             print(f"- {k.replace('smsp__pcsamp_warps_issue_stalled_', '')}: {float(x) / tot * 100:.1f}%")
         rd = to_bytes(row[h.index("dram__bytes_read.sum")], units[h.index("dram__bytes_read.sum")])
         wr = to_bytes(row[h.index("dram__bytes_write.sum")], units[h.index("dram__bytes_write.sum")])
-        print(f"\nDRAM traffic per launch: {rd + wr:.4g} bytes (read {rd:.4g}, write {wr:.4g})\n")
+        print(f"\nDRAM traffic per launch: {rd + wr:.4g} bytes (read {rd:.4g}, write {wr:.4g})")
+        l2 = None
+        if "lts__t_sectors.sum" in h:
+            l2 = float(row[h.index("lts__t_sectors.sum")].replace(",", "")) * 32.0
+            t_ms = float(row[h.index("gpu__time_duration.sum")].replace(",", ""))
+            t_s = t_ms * {"ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6, "ns": 1e-9, "nsecond": 1e-9}.get(
+                units[h.index("gpu__time_duration.sum")], 1e-3)
+            print(f"L2 traffic per launch: {l2:.4g} bytes (lts__t_sectors x 32 B) = {l2 / t_s / 1e9:.0f} GB/s")
+        print()
         if a.traffic_json:
             with open(a.traffic_json, "w") as f:
                 json.dump({"kernel": row[name_i][:100], "dram_bytes_per_launch": rd + wr, "dram_read": rd,
-                           "dram_write": wr, "report": a.rep}, f, indent=1)
+                           "dram_write": wr, "l2_bytes_per_launch": l2, "report": a.rep}, f, indent=1)
     if a.launches:
         rows = list(csv.reader(open(a.launches)))
         hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
