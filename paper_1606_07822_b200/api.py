@@ -129,7 +129,8 @@ def build_vocabulary_file(path: str, min_count: int, device: int | None = None) 
     buf = C.create_string_buffer(int(lib.cg_corpus_word_bytes(h)) + 1)
     check(lib.cg_corpus_export_vocab(h, ptr(counts, C.c_int64), buf))
     words = buf.raw[: lib.cg_corpus_word_bytes(h)].split(b"\0")[:v]
-    return Vocabulary(counts, [w.decode() for w in words], int(lib.cg_corpus_total_tokens(h)), _handle=h)
+    return Vocabulary(counts, [w.decode("utf-8", "surrogateescape") for w in words], int(lib.cg_corpus_total_tokens(h)),
+                      _handle=h)
 
 
 def read_id_stream(path: str, vocab: Vocabulary, device: int | None = None) -> np.ndarray:

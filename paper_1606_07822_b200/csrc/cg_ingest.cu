@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -287,6 +288,16 @@ void dfree(T*& p) {
     p = nullptr;
 }
 
+// Chunk size of the file reader; CG_INGEST_CHUNK (bytes, >= 64) overrides it so tests can
+// exercise many chunks and the token-longer-than-a-chunk path on small files.
+size_t chunk_bytes(size_t dflt) {
+    if (const char* e = std::getenv("CG_INGEST_CHUNK")) {
+        const long long v = std::atoll(e);
+        if (v >= 64) return static_cast<size_t>(v);
+    }
+    return dflt;
+}
+
 unsigned grid_of(uint64_t n) { return static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148ull * 16)); }
 
 // Streams a file through pinned double buffers; each delivered chunk ends at a
@@ -364,6 +375,8 @@ private:
     uint64_t pos_ = 0;
 
     void grow(int which, size_t have) {
+        // the other buffer may still feed an asynchronous H2D copy: let it land first
+        cudaDeviceSynchronize();
         const size_t ncap = cap_ * 2;
         for (int k = 0; k < 2; ++k) {
             unsigned char* nb = static_cast<unsigned char*>(cgint::PinnedPool::get().alloc(ncap));
@@ -428,8 +441,8 @@ void WordTableHost::build(const std::vector<std::string>& words) {
 int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, uint64_t capacity, cudaStream_t st,
                    IngestStats* stats) {
     const auto t0 = std::chrono::steady_clock::now();
-    constexpr size_t kChunk = size_t{32} << 20;  // small enough that reading overlaps tokenising
-    ChunkReader rd(path, kChunk);
+    // small enough that reading overlaps tokenising (CG_INGEST_CHUNK overrides, for tests)
+    ChunkReader rd(path, chunk_bytes(size_t{32} << 20));
     unsigned char* dbytes[2] = {nullptr, nullptr};
     int32_t* tmp = nullptr;
     uint32_t* tcount = nullptr;
@@ -536,8 +549,7 @@ struct DevCountTable {
 
 std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestStats* stats) {
     const auto t0 = std::chrono::steady_clock::now();
-    constexpr size_t kChunk = size_t{64} << 20;
-    ChunkReader rd(path, kChunk);
+    ChunkReader rd(path, chunk_bytes(size_t{64} << 20));
     unsigned char* dbytes[2] = {nullptr, nullptr};
     size_t dcap = 0;
     DevCountTable tab;

@@ -115,3 +115,22 @@ def test_train_from_file_is_bit_exact(tmp_path):
     s0, s1, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
     assert np.array_equal(m.syn0.view(np.uint32), s0.view(np.uint32))
     assert np.array_equal(m.syn1.view(np.uint32), s1.view(np.uint32))
+
+
+@pytest.mark.parametrize("chunk", [64, 1000, 4097])
+def test_tiny_chunks_and_tokens_longer_than_a_chunk(tmp_path, monkeypatch, chunk):
+    """Many chunks, and tokens longer than a whole chunk (the reader grows its buffers),
+    through both GPU paths; bytes beyond ASCII are ordinary token bytes."""
+    monkeypatch.setenv("CG_INGEST_CHUNK", str(chunk))
+    rng = np.random.default_rng(chunk)
+    toks = [f"t{int(r)}" for r in rng.zipf(1.2, 20000) % 500]
+    for pos in (7, 5000, 19000):
+        toks[pos] = "L" * 3000 + str(pos)  # longer than the chunk
+    toks[11] = "café"
+    toks[12] = "über"
+    text = "".join(t + (" " if i % 17 else "\n") for i, t in enumerate(toks))
+    p = tmp_path / "u.txt"
+    p.write_bytes(text.encode("utf-8") + b"\xff\xfe tail")
+    host, gpu = _vocab_pair(p, 1)
+    _same_vocab(host, gpu)
+    assert np.array_equal(api.read_id_stream(str(p), host), api.read_id_stream(str(p), host, device=0))
