@@ -14,6 +14,9 @@
 #include <memory>
 #include <atomic>
 #include <barrier>
+#include <condition_variable>
+#include <deque>
+#include <exception>
 #include <mutex>
 #include <thread>
 #include <stdexcept>
@@ -244,6 +247,93 @@ cgk::DetModel det_model(const cg_session& s) {
     m.sigmoid = s.sigmoid.p;
     m.sig_scale = host_sig_scale();
     return m;
+}
+
+// ---- host <-> device copies for pageable host memory ---------------------------------
+// A plain cudaMemcpy from/to pageable memory is staged by the driver at ~5 GB/s (23 ms
+// for the C2 model), and fresh user pages fault on first touch. Large pageable copies go
+// through two pooled pinned buffers instead, with the host-side memcpy split over
+// threads and overlapped with the DMA of the next chunk.
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    constexpr size_t kMin = size_t{2} << 20;
+    const size_t nt = std::min<size_t>(8, std::max<size_t>(1, n / kMin));
+    if (nt <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const size_t per = (n + nt - 1) / nt;
+    for (size_t t = 1; t < nt; ++t) {
+        const size_t b = t * per, e = std::min(n, b + per);
+        if (b < e) th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b); });
+    }
+    std::memcpy(dst, src, std::min(n, per));
+    for (auto& x : th) x.join();
+}
+
+constexpr size_t kStageBytes = size_t{16} << 20;
+
+void copy_to_host(void* dst, const void* dev_src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (bytes < (size_t{4} << 20) || is_pinned(dst)) {
+        CG_CUDA(cudaMemcpyAsync(dst, dev_src, bytes, cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    char* stage[2] = {static_cast<char*>(cgint::PinnedPool::get().alloc(kStageBytes)),
+                      static_cast<char*>(cgint::PinnedPool::get().alloc(kStageBytes))};
+    cudaEvent_t ev[2];
+    for (auto& e : ev) CG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    const size_t chunks = (bytes + kStageBytes - 1) / kStageBytes;
+    auto issue = [&](size_t c) {
+        const size_t b = c * kStageBytes, n = std::min(kStageBytes, bytes - b);
+        CG_CUDA(cudaMemcpyAsync(stage[c & 1], static_cast<const char*>(dev_src) + b, n, cudaMemcpyDeviceToHost, st));
+        CG_CUDA(cudaEventRecord(ev[c & 1], st));
+    };
+    issue(0);
+    for (size_t c = 0; c < chunks; ++c) {
+        if (c + 1 < chunks) issue(c + 1);  // stage[(c+1)&1] was drained in iteration c-1
+        CG_CUDA(cudaEventSynchronize(ev[c & 1]));
+        const size_t b = c * kStageBytes;
+        parallel_memcpy(static_cast<char*>(dst) + b, stage[c & 1], std::min(kStageBytes, bytes - b));
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto* p : stage) cgint::PinnedPool::get().free(p);
+}
+
+void copy_to_device(void* dev_dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return;
+    if (bytes < (size_t{4} << 20) || is_pinned(src)) {
+        CG_CUDA(cudaMemcpyAsync(dev_dst, src, bytes, cudaMemcpyHostToDevice, st));
+        return;
+    }
+    char* stage[2] = {static_cast<char*>(cgint::PinnedPool::get().alloc(kStageBytes)),
+                      static_cast<char*>(cgint::PinnedPool::get().alloc(kStageBytes))};
+    cudaEvent_t ev[2];
+    for (auto& e : ev) CG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    const size_t chunks = (bytes + kStageBytes - 1) / kStageBytes;
+    for (size_t c = 0; c < chunks; ++c) {
+        const int k = static_cast<int>(c & 1);
+        if (used[k]) CG_CUDA(cudaEventSynchronize(ev[k]));  // its previous DMA has finished
+        const size_t b = c * kStageBytes, n = std::min(kStageBytes, bytes - b);
+        parallel_memcpy(stage[k], static_cast<const char*>(src) + b, n);
+        CG_CUDA(cudaMemcpyAsync(static_cast<char*>(dev_dst) + b, stage[k], n, cudaMemcpyHostToDevice, st));
+        CG_CUDA(cudaEventRecord(ev[k], st));
+        used[k] = true;
+    }
+    CG_CUDA(cudaStreamSynchronize(st));
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (auto* p : stage) cgint::PinnedPool::get().free(p);
 }
 
 void session_reset_model(cg_session& s) {
@@ -554,7 +644,8 @@ int cg_session_upload_ids(cg_session* s, const int32_t* ids, int64_t n_ids) {
     return guarded([&] {
         if (n_ids < 0) invalid("negative id count");
         CG_CUDA(cudaSetDevice(s->device));
-        s->ids.upload(ids, static_cast<size_t>(n_ids), s->stream);
+        s->ids.alloc(static_cast<size_t>(n_ids));
+        copy_to_device(s->ids.p, ids, static_cast<size_t>(n_ids) * sizeof(int32_t), s->stream);
         session_alloc_stream(s, n_ids);
         check_ids_on_device(s);
     });
@@ -606,15 +697,15 @@ int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out) {
         CG_CUDA(cudaSetDevice(s->device));
         const size_t n0 = static_cast<size_t>(s->V) * s->D, n1 = static_cast<size_t>(s->V - 1) * s->D;
         if (s->mode == CG_MODE_DETERMINISTIC) {
-            if (syn0_out) CG_CUDA(cudaMemcpyAsync(syn0_out, s->syn0(), n0 * 4, cudaMemcpyDeviceToHost, s->stream));
-            if (syn1_out) CG_CUDA(cudaMemcpyAsync(syn1_out, s->syn1(), n1 * 4, cudaMemcpyDeviceToHost, s->stream));
+            if (syn0_out) copy_to_host(syn0_out, s->syn0(), n0 * 4, s->stream);
+            if (syn1_out) copy_to_host(syn1_out, s->syn1(), n1 * 4, s->stream);
         } else {
             if (s->stage.n < n0 + n1) s->stage.alloc(n0 + n1);
             gather_rows_kernel<<<grid_for(static_cast<int64_t>(n0)), 256, 0, s->stream>>>(s->stage.p, s->D, s->syn0(), s->Dp, nullptr, s->V, s->D);
             gather_rows_kernel<<<grid_for(static_cast<int64_t>(n1)), 256, 0, s->stream>>>(s->stage.p + n0, s->D, s->syn1(), s->Dp, s->row_of_node_dev.p, s->V - 1, s->D);
             CG_CUDA(cudaGetLastError());
-            if (syn0_out) CG_CUDA(cudaMemcpyAsync(syn0_out, s->stage.p, n0 * 4, cudaMemcpyDeviceToHost, s->stream));
-            if (syn1_out) CG_CUDA(cudaMemcpyAsync(syn1_out, s->stage.p + n0, n1 * 4, cudaMemcpyDeviceToHost, s->stream));
+            if (syn0_out) copy_to_host(syn0_out, s->stage.p, n0 * 4, s->stream);
+            if (syn1_out) copy_to_host(syn1_out, s->stage.p + n0, n1 * 4, s->stream);
         }
         CG_CUDA(cudaStreamSynchronize(s->stream));
     });
@@ -1197,6 +1288,129 @@ int cg_session_load_corpus(cg_session* s, const char* path, const char* words_nu
     });
 }
 
+}  // extern "C"
+
+namespace {
+// Hands the ingest's per-chunk progress (an event and a pinned word with the ids written
+// so far) from the tokenising thread to the training thread.
+struct ChunkQueue {
+    static constexpr int kBlock = 1024;
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::pair<int, cudaEvent_t>> q;
+    std::vector<uint64_t*> blocks;
+    bool done = false;
+    uint64_t* word(int j) {
+        std::lock_guard<std::mutex> g(mu);
+        while (static_cast<int>(blocks.size()) * kBlock <= j)
+            blocks.push_back(static_cast<uint64_t*>(cgint::PinnedPool::get().alloc(kBlock * sizeof(uint64_t))));
+        return blocks[static_cast<size_t>(j / kBlock)] + j % kBlock;
+    }
+    ~ChunkQueue() {
+        for (auto& it : q) cudaEventDestroy(it.second);
+        for (uint64_t* b : blocks) cgint::PinnedPool::get().free(b);
+    }
+};
+uint64_t* chunk_word(void* ctx, int j) { return static_cast<ChunkQueue*>(ctx)->word(j); }
+void chunk_ready(void* ctx, int j, cudaEvent_t ev) {
+    auto* q = static_cast<ChunkQueue*>(ctx);
+    {
+        std::lock_guard<std::mutex> g(q->mu);
+        q->q.emplace_back(j, ev);
+    }
+    q->cv.notify_one();
+}
+
+// train(corpus_path) in Hogwild mode with the first pass overlapped with tokenisation:
+// a host thread streams and tokenises the file into the session's id buffer while this
+// thread trains every chunk as soon as its ids have landed (K3 + K1 per chunk; the draws
+// are keyed by global token index, so only the sentence cuts at chunk edges differ from
+// one launch over the whole stream). Later passes run over the whole stream. Returns
+// false -- nothing trained that matters -- if the file holds more in-vocabulary tokens
+// than the vocabulary counted (then the caller re-runs the sequential path).
+bool train_file_pipelined(cg_session* s, const char* path, const std::vector<std::string>& words,
+                          cg_train_stats* out) {
+    CG_CUDA(cudaSetDevice(s->device));
+    DevWordTable table;
+    table.upload(words, s->stream);
+    const uint64_t cap = static_cast<uint64_t>(std::max<int64_t>(s->total_tokens, 0)) + 4096;
+    s->ids.alloc(cap);
+    session_alloc_stream(s, static_cast<int64_t>(cap));  // K3 buffers fit any chunk
+    ChunkQueue q;
+    cgk::IngestProgress prog{chunk_word, chunk_ready, &q};
+    cudaStream_t ist = nullptr;
+    CG_CUDA(cudaStreamCreateWithFlags(&ist, cudaStreamNonBlocking));
+    int64_t total = -1;
+    std::exception_ptr perr;
+    std::thread producer([&] {
+        try {
+            CG_CUDA(cudaSetDevice(s->device));
+            total = cgk::ingest_ids(path, table.view, s->ids.p, cap, ist, nullptr, &prog);
+        } catch (...) {
+            perr = std::current_exception();
+        }
+        {
+            std::lock_guard<std::mutex> g(q.mu);
+            q.done = true;
+        }
+        q.cv.notify_one();
+    });
+    cg_train_stats st{};
+    uint64_t trained = 0;
+    bool overflow = false;
+    std::string err;
+    int err_rc = CG_OK;
+    for (;;) {
+        std::pair<int, cudaEvent_t> item{-1, nullptr};
+        {
+            std::unique_lock<std::mutex> g(q.mu);
+            q.cv.wait(g, [&] { return !q.q.empty() || q.done; });
+            if (q.q.empty()) break;
+            item = q.q.front();
+            q.q.pop_front();
+        }
+        cudaEventSynchronize(item.second);
+        cudaEventDestroy(item.second);
+        const uint64_t c = *q.word(item.first);
+        if (c > cap) overflow = true;
+        if (overflow || err_rc != CG_OK || c <= trained) continue;
+        cg_epoch_stats e{};
+        const int rc = cg_session_train_range(s, 0, static_cast<int64_t>(trained), static_cast<int64_t>(c), trained, 1, &e);
+        if (rc != CG_OK) {
+            err_rc = rc;
+            err = g_error;
+            continue;
+        }
+        st.kernel_seconds += (e.train_ms + e.subsample_ms) * 1e-3;
+        st.centers += e.kept;
+        st.pairs += e.pairs;
+        st.steps += e.steps;
+        st.words_processed += e.words;
+        trained = c;
+    }
+    producer.join();
+    cudaStreamDestroy(ist);
+    if (perr) std::rethrow_exception(perr);
+    if (err_rc != CG_OK) throw CgError(err_rc, err);
+    if (overflow || static_cast<uint64_t>(total) > cap) return false;
+    s->n_ids = total;
+    for (int32_t it = 1; it < s->cfg.iterations; ++it) {
+        cg_epoch_stats e{};
+        const int rc = cg_session_train_range(s, it, 0, total, static_cast<uint64_t>(it) * static_cast<uint64_t>(total), 1, &e);
+        if (rc != CG_OK) throw CgError(rc, g_error);
+        st.kernel_seconds += (e.train_ms + e.subsample_ms) * 1e-3;
+        st.centers += e.kept;
+        st.pairs += e.pairs;
+        st.steps += e.steps;
+        st.words_processed += e.words;
+    }
+    *out = st;
+    return true;
+}
+}  // namespace
+
+extern "C" {
+
 int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const char* corpus_path,
                   const char* words_nul, float* syn0_out, float* syn1_out, cg_train_stats* stats) {
     cg_session* s = nullptr;
@@ -1205,13 +1419,28 @@ int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc* model
         cudaGetLastError();
         dev = 0;
     }
+    const auto tc = std::chrono::steady_clock::now();
     int rc = cg_session_create(cfg, mode, model, dev, nullptr, &s);
     if (rc != CG_OK) return rc;
     const auto t0 = std::chrono::steady_clock::now();
-    rc = cg_session_load_corpus(s, corpus_path, words_nul, nullptr);
     cg_train_stats st{};
-    if (rc == CG_OK) rc = cg_session_train(s, &st);
+    bool done = false;
+    if (mode == CG_MODE_HOGWILD && corpus_path && words_nul) {
+        rc = guarded([&] { done = train_file_pipelined(s, corpus_path, split_nul(words_nul, s->V), &st); });
+        if (rc == CG_OK && !done) rc = cg_session_reset_model(s);  // undercounted vocabulary: start over
+    }
+    if (rc == CG_OK && !done) {
+        rc = cg_session_load_corpus(s, corpus_path, words_nul, nullptr);
+        if (rc == CG_OK) rc = cg_session_train(s, &st);
+    }
+    const auto t1 = std::chrono::steady_clock::now();
     if (rc == CG_OK) rc = cg_session_download(s, syn0_out, syn1_out);
+    if (std::getenv("CG_PROFILE")) {
+        const auto t2 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        std::fprintf(stderr, "cg_train_file: create %.2f ms, ingest+train %.2f ms (kernels %.2f, %s), download %.2f ms\n",
+                     ms(tc, t0), ms(t0, t1), st.kernel_seconds * 1e3, done ? "pipelined" : "sequential", ms(t1, t2));
+    }
     // like the reference's, the wall time covers reading the corpus as well as training
     st.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     st.words_per_second = st.wall_seconds > 0 ? static_cast<double>(st.words_processed) / st.wall_seconds : 0.0;

@@ -439,7 +439,7 @@ void WordTableHost::build(const std::vector<std::string>& words) {
 }
 
 int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, uint64_t capacity, cudaStream_t st,
-                   IngestStats* stats) {
+                   IngestStats* stats, const IngestProgress* progress) {
     const auto t0 = std::chrono::steady_clock::now();
     // small enough that reading overlaps tokenising (CG_INGEST_CHUNK overrides, for tests)
     ChunkReader rd(path, chunk_bytes(size_t{32} << 20));
@@ -471,7 +471,7 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
     for (auto& e : done) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     bool used[2] = {false, false};
     uint64_t bytes_total = 0;
-    int k = 0;
+    int k = 0, chunk = 0;
     try {
         for (;; k ^= 1) {
             if (used[k]) check(cudaEventSynchronize(done[k]), "event sync");  // host buffer k free again
@@ -491,6 +491,15 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
             check(cudaEventRecord(done[k], st), "event");
             used[k] = true;
             if (stats) stats->launches += 4;
+            if (progress) {
+                uint64_t* w = progress->word(progress->ctx, chunk);
+                check(cudaMemcpyAsync(w, cursor, sizeof(uint64_t), cudaMemcpyDeviceToHost, st), "D2H");
+                cudaEvent_t ev;
+                check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+                check(cudaEventRecord(ev, st), "event");
+                progress->on_chunk(progress->ctx, chunk, ev);
+            }
+            ++chunk;
         }
         uint64_t total = 0;
         check(cudaMemcpyAsync(&total, cursor, sizeof total, cudaMemcpyDeviceToHost, st), "D2H");

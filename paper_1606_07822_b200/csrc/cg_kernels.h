@@ -205,8 +205,17 @@ unsigned long long host_token_hash(const char* s, size_t len);
 // Tokenises a corpus file on the device; in-vocabulary ids are written in file order to
 // out[0..capacity) (device). Returns the number of in-vocabulary tokens (which may exceed
 // capacity: then only the first `capacity` were written).
+// Per-chunk progress: after chunk j is queued, the number of ids written so far is copied
+// (asynchronously) into the pinned host word word(ctx, j) provided by the receiver, and
+// on_chunk(ctx, j, ev) hands over an event that completes after that copy (the receiver
+// destroys it).
+struct IngestProgress {
+    uint64_t* (*word)(void* ctx, int chunk);
+    void (*on_chunk)(void* ctx, int chunk, cudaEvent_t ev);
+    void* ctx;
+};
 int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, uint64_t capacity, cudaStream_t st,
-                   IngestStats* stats);
+                   IngestStats* stats, const IngestProgress* progress = nullptr);
 // Counts every distinct token of a corpus file on the device (unordered).
 std::vector<CountedWord> ingest_count(const char* path, cudaStream_t st, IngestStats* stats);
 

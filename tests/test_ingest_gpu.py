@@ -134,3 +134,38 @@ def test_tiny_chunks_and_tokens_longer_than_a_chunk(tmp_path, monkeypatch, chunk
     host, gpu = _vocab_pair(p, 1)
     _same_vocab(host, gpu)
     assert np.array_equal(api.read_id_stream(str(p), host), api.read_id_stream(str(p), host, device=0))
+
+
+def test_hogwild_train_from_file_pipelined(tmp_path, monkeypatch):
+    """train(corpus_path) in Hogwild mode trains the first pass chunk by chunk while the
+    file is still being tokenised: every token is covered once per pass, and the model
+    learns as much as training from the id stream. A vocabulary that undercounts the
+    file (built from a prefix) falls back to the sequential path and still covers it."""
+    monkeypatch.setenv("CG_INGEST_CHUNK", "65536")  # several chunks on a small file
+    path = F.write(tmp_path / "h.txt", F.make_zipf_corpus(400_000, 2000, 13))
+    vocab = api.build_vocabulary_file(path, 1)
+    ids = api.read_id_stream(path, vocab)
+    tree = api.build_huffman_tree(vocab)
+    sel = api.select_cached_nodes(tree, 31)
+    cfg = dict(dim=24, window=5, min_count=1, sample=1e-3, iterations=2, cache_nodes=31, seed=3)
+    tc = api.TrainConfig(**cfg, mode="hogwild")
+    st = api.TrainStats()
+    m_file = api.train(path, vocab, tree, sel, tc, st)
+    assert st.words_processed == 2 * ids.size
+    m_ids = api.train(ids, vocab, tree, sel, tc)
+    t = O.Tree(tree.offsets, tree.nodes, tree.turns, tree.usage)
+    cen, ctx = O.sample_pairs(ids, vocab.counts, vocab.total_tokens(), 1e-3, 5, 7, 1 << 16)
+    init = api.init_model(vocab.size(), 24, 3)
+    l0, lf, li = (O.hs_loss(cen, ctx, m.syn0, m.syn1, t) for m in (init, m_file, m_ids))
+    assert lf < l0 and abs((l0 - lf) - (l0 - li)) < 0.05 * (l0 - li), (l0, lf, li)
+    # undercounting vocabulary: counts from the first half of the file only
+    half = tmp_path / "half.txt"
+    half.write_text(open(path).read()[: 200_000])
+    small = api.build_vocabulary_file(str(half), 1)
+    ids_small = api.read_id_stream(path, small)
+    assert ids_small.size > small.total_tokens()
+    tree2 = api.build_huffman_tree(small)
+    st2 = api.TrainStats()
+    m2 = api.train(path, small, tree2, api.select_cached_nodes(tree2, 31), tc, st2)
+    assert st2.words_processed == 2 * ids_small.size
+    assert np.isfinite(m2.syn0).all()
