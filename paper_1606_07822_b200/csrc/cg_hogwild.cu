@@ -712,7 +712,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 
 // v4 rows per group and worker warps per CTA. G = 8 measured worse: for D <= 128 (C1 K1
 // 3.66 -> 4.48 ms, 11 workers: ptxas budgets registers for a multiple of 4 warps, so 13
-// workers would get 128 and spill) and for D <= 256 (C2 90 -> 124 ms, 7 workers).
+// workers would get 128 and spill) and for D <= 256 (C2 90 -> 124 ms, 7 workers); G = 2
+// with 15 workers (128 registers, context batch 7) is also slower at C2 (116 ms).
 template <int DCH>
 constexpr int kG4 = 4;
 template <int DCH>
