@@ -56,6 +56,7 @@ def parse():
     p.add_argument("--cold-update", type=int, default=0)
     p.add_argument("--hot-flush-scale", type=float, default=0.0)
     p.add_argument("--kernel", type=int, default=0, help="K1 version: 0 default, 3 = v3 per-context kernel")
+    p.add_argument("--probe", type=int, default=0, help="K1 experiment bits (cg_tuning.probe); 0 for real runs")
     return p.parse_args()
 
 
@@ -281,7 +282,8 @@ def main():
                           cache_nodes=args.cache_nodes, seed=c.seed, mode="hogwild")
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
-    sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale, kernel=args.kernel)
+    sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale, kernel=args.kernel,
+              probe=args.probe)
     if isinstance(ids, np.ndarray):
         sess.upload_ids(ids)
     else:

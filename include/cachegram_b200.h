@@ -177,6 +177,10 @@ typedef struct cg_epoch_stats {
     double subsample_ms;     /* device time of subsampling + compaction */
     int32_t train_launches;  /* kernels launched by this call */
     int32_t other_launches;
+    int32_t cached_rows;     /* hogwild: syn1 rows held in each CTA's shared-memory cache */
+    int32_t worker_warps;    /* hogwild: worker warps per CTA */
+    int32_t ctx_batch;       /* hogwild: contexts staged per batch */
+    int32_t blocks;          /* hogwild: persistent CTAs */
 } cg_epoch_stats;
 
 /* stream: a cudaStream_t (NULL = legacy default stream). device: CUDA ordinal. */

@@ -83,6 +83,10 @@ class CgEpochStats(C.Structure):
         ("subsample_ms", C.c_double),
         ("train_launches", C.c_int32),
         ("other_launches", C.c_int32),
+        ("cached_rows", C.c_int32),
+        ("worker_warps", C.c_int32),
+        ("ctx_batch", C.c_int32),
+        ("blocks", C.c_int32),
     ]
 
 

@@ -849,6 +849,10 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             out.steps = cnt[2];
             out.train_launches = 1;
             out.other_launches = sub_launches;
+            out.cached_rows = g.cache_rows;
+            out.worker_warps = g.warps;
+            out.ctx_batch = g.ctx_batch;
+            out.blocks = g.blocks;
             if (cnt[3] != kept) throw CgError(CG_ERR_INTERNAL, "hogwild kernel did not cover every kept center");
         }
         if (st) *st = out;

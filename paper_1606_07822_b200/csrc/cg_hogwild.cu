@@ -379,16 +379,24 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog_kernel(HogArgs a) {
 }
 
 // ---- K1 v4: center-batched row groups ---------------------------------------------
+// Lane q = lane + 32 k of chunk k is inside a row of d4 float4: chunks k < DCH - 1 always
+// are (the variant is DCH = ceil(d4 / 32)), so only the last chunk needs the predicate.
+template <int DCH>
+__device__ __forceinline__ bool in_row(int k, int q, int d4) {
+    return k < DCH - 1 || q < d4;
+}
+
 // Learning signals of CIc contexts (cc .., clamped to the batch) against the G rows in U:
 // the CIc*G dot products are reduced together (transpose-reduce), after which the pair
-// (ii, g) lives in lane (ii*G + g) << (5 - log2(CIc*G)); each lane returns its pair's
-// g = (1 - turn - sigmoid(dot)) * alpha, or 0 for a padded context / row.
+// (ii, g) lives in lane (ii*G + g) << (5 - log2(CIc*G)); that lane evaluates the pair's
+// g = (1 - turn - sigmoid(dot)) * alpha (0 for a padded context / row) and stores it at
+// sg[ii*G + g], so the update loop fetches a context's G signals with one broadcast load.
 template <int DCH, int G, int CIc>
-__device__ __forceinline__ float chunk_signal(const float4* V, int d4, int lane, int cc, int nb,
-                                              const float4 (&U)[G][DCH], const int* codes, int j0, int L,
-                                              const float* sig, float sig_scale, float alpha) {
+__device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, int cc, int nb,
+                                             const float4 (&U)[G][DCH], const int* codes, int j0, int L,
+                                             const float* sig, float sig_scale, float alpha, float* sg) {
     constexpr int N = CIc * G;
-    constexpr int LN = Log2<N>::v, LGG = Log2<G>::v;
+    constexpr int LN = Log2<N>::v, LGG = Log2<G>::v, LS = 5 - LN;
     float p[N];
 #pragma unroll
     for (int ii = 0; ii < CIc; ++ii) {
@@ -408,11 +416,14 @@ __device__ __forceinline__ float chunk_signal(const float4* V, int d4, int lane,
         }
     }
     const float tot = transpose_reduce<N>(p, lane);
-    const int vi = lane >> (5 - LN);
+    const int vi = lane >> LS;
     const int my_i = vi >> LGG, my_g = vi & (G - 1);
     const int code = codes[j0 + my_g];
     const float f = table_sigmoid(sig, tot, sig_scale);
-    return (j0 + my_g < L && cc + my_i < nb) ? (1.0f - static_cast<float>(code & 1) - f) * alpha : 0.f;
+    const float gl = (j0 + my_g < L && cc + my_i < nb) ? (1.0f - static_cast<float>(code & 1) - f) * alpha : 0.f;
+    __syncwarp();  // every lane has read the previous chunk's signals
+    if ((lane & ((1 << LS) - 1)) == 0) sg[vi] = gl;
+    __syncwarp();
 }
 
 // Same persistent/ticket/flusher structure, smem layout and hot-row cache protocol as
@@ -425,8 +436,12 @@ __device__ __forceinline__ float chunk_signal(const float4* V, int d4, int lane,
 // each lane evaluates one sigmoid, and the updates (h_i += g U, delta += g v) follow as
 // pure FMA streams. This removes v3's serial dot -> reduce -> sigmoid -> update chain per
 // (context, group), the latency that held issue at ~46% with 12 warps per SM.
+// Workers arrive on a shared-memory mbarrier once per merged center; the flusher polls
+// it (test_wait) and drains the cache whenever `flush_centers` merges have completed a
+// phase, and once more when the workers are done.
 template <int DCH, int G, int WORKERS>
 __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) {
+    static_assert(G == 4, "signals are fetched as one float4 per context");
     extern __shared__ float4 hsm[];
     float* sig = reinterpret_cast<float*>(hsm);
     int* codes_all = reinterpret_cast<int*>(hsm + 256);
@@ -437,7 +452,8 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     float4* ctx_all = reinterpret_cast<float4*>(locks + ((K + 3) & ~3));
     const int NB = a.ctx_batch;
     __shared__ int s_done;
-    __shared__ unsigned s_merged;
+    __shared__ uint64_t s_bar;
+    __shared__ float4 s_sig[WORKERS * 8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int workers = (blockDim.x >> 5) - 1;
@@ -450,17 +466,22 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     }
     if (tid == 0) {
         s_done = 0;
-        s_merged = 0;
+        mbar_init(&s_bar, static_cast<unsigned>(a.flush_centers));
     }
     __syncthreads();
 
-    if (warp == workers) {  // flusher, as in hog_kernel
-        unsigned last = 0;
+    if (warp == workers) {  // flusher
+        if (K == 0) return;  // nothing cached, nothing to flush
+        unsigned phase = 0;
         for (;;) {
+            // Due once flush_centers merges have completed the barrier's phase. Polled
+            // every ~20 us: sleeping in try_wait (suspend-time hint) until the phase
+            // completes measured slower (C2 K1 90.3 vs 84.7 ms, C3 156 vs 137 ms).
+            __nanosleep(20000);
+            const bool due = mbar_test_wait(&s_bar, phase);
+            if (due) phase ^= 1u;
             const bool done = *reinterpret_cast<volatile int*>(&s_done) == workers;
-            const unsigned merged = *reinterpret_cast<volatile unsigned*>(&s_merged);
-            if (K > 0 && (done || merged - last >= static_cast<unsigned>(a.flush_centers))) {
-                last = merged;
+            if (due || done) {
                 for (int r = 0; r < K; ++r) {
                     if (lane == 0)
                         while (atomicCAS(&locks[r], 0, 1) != 0) {
@@ -472,7 +493,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
                         d[k] = f4(0.f);
-                        if (q < d4) {
+                        if (in_row<DCH>(k, q, d4)) {
                             d[k] = dblk[r * d4 + q];
                             dblk[r * d4 + q] = f4(0.f);
                         }
@@ -484,21 +505,18 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
-                        if (q < d4 && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
+                        if (in_row<DCH>(k, q, d4) && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
                     }
                 }
                 __threadfence();
             }
             if (done) break;
-            // Poll rarely: a flush is due every ~0.4 ms (128 centers over the CTA's warps),
-            // and nanosleep may return early (PTX: anywhere in [0, 2t]). At 2 us the polling
-            // loop was 6% of all instructions issued on the SM (ncu, C2).
-            __nanosleep(20000);
         }
         return;
     }
 
     int* codes = codes_all + warp * kCodeSlots;
+    float* sg = reinterpret_cast<float*>(s_sig + warp * 8);
     float4* V = ctx_all + static_cast<size_t>(warp) * 2 * NB * d4;
     float4* Hs = V + NB * d4;
     // per-warp staging of the next row group (cp.async one group ahead of its use)
@@ -510,13 +528,14 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
             for (int k = 0; k < DCH; ++k) {
                 const int q = lane + 32 * k;
-                if (q < d4) cp_async16(Ub + g * d4 + q, a.syn1 + 4 * (rg * d4 + q));
+                if (in_row<DCH>(k, q, d4)) cp_async16(Ub + g * d4 + q, a.syn1 + 4 * (rg * d4 + q));
             }
         }
     };
     const int dummy_code = a.dummy_row << 1;
     const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
     const int cpw = a.centers_per_warp;
+    const bool cache_reads = !(a.probe & 8), cold_writes = !(a.probe & 1), ctx_writes = !(a.probe & 2);
     unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
 
     for (;;) {
@@ -569,7 +588,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
                         const int q = lane + 32 * k;
-                        if (q < d4) {
+                        if (in_row<DCH>(k, q, d4)) {
                             cp_async16(V + i * d4 + q, a.syn0 + 4 * (xo + q));
                             Hs[i * d4 + q] = f4(0.f);
                         }
@@ -586,13 +605,21 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                         for (int k = 0; k < DCH; ++k) {
                             const int q = lane + 32 * k;
-                            float4 u = f4(0.f);
-                            if (q < d4) {
-                                u = Ub[g * d4 + q];
-                                if (row[g] < K && !(a.probe & 8)) u = add4(u, dblk[row[g] * d4 + q]);  // + this CTA's cached delta
-                            }
-                            U[g][k] = u;
+                            U[g][k] = in_row<DCH>(k, q, d4) ? Ub[g * d4 + q] : f4(0.f);
                             Dl[g][k] = f4(0.f);
+                        }
+                    }
+                    // + this CTA's cached delta; row[g] is warp-uniform, so is the branch
+                    if (cache_reads) {
+#pragma unroll
+                        for (int g = 0; g < G; ++g) {
+                            if (row[g] < K) {
+#pragma unroll
+                                for (int k = 0; k < DCH; ++k) {
+                                    const int q = lane + 32 * k;
+                                    if (in_row<DCH>(k, q, d4)) U[g][k] = add4(U[g][k], dblk[row[g] * d4 + q]);
+                                }
+                            }
                         }
                     }
                     __syncwarp();  // every lane has its copy: Ub takes the next group
@@ -602,21 +629,17 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                         // covered without computing dots for padding (a fixed 8 wasted ~40%)
                         const int r = nb - cc;
                         constexpr int CIM = 32 / G;  // contexts per full chunk (CIM * G = 32 dots)
-                        float gl;
-                        int ls, cic;
+                        int cic;
                         if (r >= CIM) {
-                            gl = chunk_signal<DCH, G, CIM>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha);
-                            ls = 5 - Log2<CIM * G>::v;
+                            chunk_signal<DCH, G, CIM>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha, sg);
                             cic = CIM;
                         } else if (r >= CIM / 2) {
-                            gl = chunk_signal<DCH, G, CIM / 2>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale,
-                                                               alpha);
-                            ls = 5 - Log2<CIM / 2 * G>::v;
+                            chunk_signal<DCH, G, CIM / 2>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha,
+                                                          sg);
                             cic = CIM / 2;
                         } else {
-                            gl = chunk_signal<DCH, G, CIM / 4>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale,
-                                                               alpha);
-                            ls = 5 - Log2<CIM / 4 * G>::v;
+                            chunk_signal<DCH, G, CIM / 4>(V, d4, lane, cc, nb, U, codes, j0, L, sig, a.sig_scale, alpha,
+                                                          sg);
                             cic = CIM / 4;
                         }
                         // Rolled: unrolled (fully or 2x), the kernel's hot loop
@@ -624,8 +647,9 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                         // no_instruction stalls fully unrolled; 2x: +11% K1 time at D 300).
                         // Lanes past the row end compute on neighbouring data; their hacc
                         // and delta chunks are never written back.
+                        const int ni = min(cic, r);
 #pragma unroll 1
-                        for (int ii = 0; ii < min(cic, r); ++ii) {
+                        for (int ii = 0; ii < ni; ++ii) {
                             const int i = cc + ii;
                             // h accumulates in place: load Hs[i] up front (with v) so the
                             // loads overlap and the FMAs add straight into it
@@ -635,9 +659,9 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                                 v[k] = V[i * d4 + lane + 32 * k];
                                 hacc[k] = Hs[i * d4 + lane + 32 * k];
                             }
-                            float gg[G];
-#pragma unroll
-                            for (int g = 0; g < G; ++g) gg[g] = __shfl_sync(kFull, gl, (ii * G + g) << ls);
+                            const float4 g4 = reinterpret_cast<const float4*>(sg)[ii];
+                            // one broadcast load instead of G shuffles: C2 K1 92.2 -> 90.3 ms
+                            const float gg[G] = {g4.x, g4.y, g4.z, g4.w};
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -649,7 +673,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
-                                if (q < d4) Hs[i * d4 + q] = hacc[k];
+                                if (in_row<DCH>(k, q, d4)) Hs[i * d4 + q] = hacc[k];
                             }
                         }
                         cc += cic;
@@ -667,7 +691,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
-                                if (q < d4) {
+                                if (in_row<DCH>(k, q, d4)) {
                                     const int e = row[g] * d4 + q;
                                     dblk[e] = add4(dblk[e], Dl[g][k]);
                                 }
@@ -675,23 +699,23 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
                             __threadfence_block();
                             __syncwarp();
                             if (lane == 0) atomicExch(&locks[row[g]], 0);
-                        } else if (!(a.probe & 1)) {
+                        } else if (cold_writes) {
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
-                                if (q < d4) red_add4(a.syn1 + 4 * (row[g] * d4 + q), Dl[g][k]);
+                                if (in_row<DCH>(k, q, d4)) red_add4(a.syn1 + 4 * (row[g] * d4 + q), Dl[g][k]);
                             }
                         }
                     }
                 }
                 __syncwarp();
-                if (!(a.probe & 2)) {
+                if (ctx_writes) {
                     for (int i = 0; i < nb; ++i) {
                         const int xo = __shfl_sync(kFull, xid, i) * d4;
 #pragma unroll
                         for (int k = 0; k < DCH; ++k) {
                             const int q = lane + 32 * k;
-                            if (q < d4) red_add4(a.syn0 + 4 * (xo + q), Hs[i * d4 + q]);
+                            if (in_row<DCH>(k, q, d4)) red_add4(a.syn0 + 4 * (xo + q), Hs[i * d4 + q]);
                         }
                     }
                 }
@@ -699,14 +723,17 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
             }
             n_pairs += static_cast<unsigned long long>(n);
             n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
-            if (lane == 0 && touched_cache) atomicAdd(&s_merged, 1u);
+            if (lane == 0 && touched_cache) mbar_arrive(&s_bar);
         }
     }
     if (lane == 0) {
         atomicAdd(a.counters + 1, n_pairs);
         atomicAdd(a.counters + 2, n_steps);
         atomicAdd(a.counters + 3, n_centers);
-        atomicAdd(&s_done, 1);
+        // the last worker completes the barrier's current phase so the flusher wakes for
+        // the final flush (arrivals past it only start the next, never-awaited phase)
+        if (atomicAdd(&s_done, 1) == workers - 1)
+            for (int i = 0; i < a.flush_centers; ++i) mbar_arrive(&s_bar);
     }
 }
 
