@@ -306,6 +306,8 @@ def main():
             agg["steps"] += e.steps
             agg["kept"] += e.kept
             agg["launch_count"] += e.train_launches
+            agg["geometry"] = {"blocks": e.blocks, "worker_warps": e.worker_warps, "ctx_batch": e.ctx_batch,
+                               "cached_rows_per_cta": e.cached_rows}
         return e
 
     from paper_1606_07822_b200.replicas import ReplicaTrainer
@@ -470,7 +472,8 @@ def main():
             "gpu_launches": launches["n"],
             "clocks": clk,
             "detail": {"pairs_per_step": agg["pairs"] / args.steps, "path_steps_per_step": agg["steps"] / args.steps,
-                       "kept_per_step": agg["kept"] / args.steps, "step_ms": step_ms},
+                       "kept_per_step": agg["kept"] / args.steps, "step_ms": step_ms,
+                       "k1_geometry": agg.get("geometry")},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -217,11 +217,14 @@ typedef struct cg_tuning {
     float hot_flush_scale;    /* 0 = per-row 1/E[#CTAs contributing per flush] (averaging of overlapping
                                  CTA replicas); > 0 = this multiplier for every cached row */
     int32_t flush_centers;    /* 0 = 128: centers merged into a CTA's cache between flushes */
-    int32_t min_cache_rows;   /* 0 = default (at least the top 31 rows are cached); < 0 = honour K exactly,
+    int32_t min_cache_rows;   /* 0 = default: each CTA caches the top 8 rows (K picks them, the top 31 rows
+                                 by usage follow); > 0 = cache max(8, this) rows, at most max(K, 31);
+                                 < 0 = honour K exactly,
                                  even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
                                  context-row updates, bit 2 skip cache merges, bit 3 skip reading the
-                                 CTA's cached deltas */
+                                 CTA's cached deltas; bit 5 (harmless) runs the generic-width K1
+                                 instead of the one specialised for D = 100/128/200/300 */
     int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);

@@ -500,7 +500,10 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
         s->stream = static_cast<cudaStream_t>(stream);
         s->V = md->vocab_size;
         s->D = cfg->dim;
-        s->Dp = (cfg->dim + 3) / 4 * 4;
+        // Hogwild rows are padded to 32 bytes (8 floats): every row -- in HBM and in the
+        // kernel's shared-memory staging -- then starts on a 32-byte boundary. Rows at
+        // 16 mod 32 made K1 ~30% slower (C1/C3, profiles/r1_smem_align.jsonl).
+        s->Dp = (cfg->dim + 7) / 8 * 8;
         s->K = md->hot_count;
         s->total_tokens = md->total_tokens;
         const int32_t V = s->V;
@@ -798,13 +801,22 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
             h.counters = s->counters.p;
             h.cold_store = s->tune.cold_update;
-            const int32_t want_rows = s->tune.min_cache_rows < 0 ? s->K : s->cached_rows;
+            // Rows each CTA caches in shared memory. By default the top kGpuCacheRows rows,
+            // whatever K is: more cached rows cost more lock/merge/flush work than the
+            // red.global of a moderately hot row, and at D 300 they cost a worker warp
+            // (K1 sweep, profiles/r1_rows_sweep.jsonl: 8 rows is within 3% of the fastest at
+            // C1-C5, 31 rows is 3-16% slower; loss unchanged). K selects the rows (the
+            // CacheSelection order); min_cache_rows < 0 honours K exactly (the K sweep).
+            constexpr int32_t kGpuCacheRows = 8;
+            const int32_t want_rows =
+                s->tune.min_cache_rows < 0 ? s->K : std::min(s->cached_rows, std::max(kGpuCacheRows, s->tune.min_cache_rows));
             h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 128;  // 32: +22% K1 time at C2, 64: +8%, 256: same as 128 (profiles/r1_perf4_c2.jsonl)
             h.dummy_row = s->V - 1;
             h.probe = s->tune.probe;
-            const cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
-                                                     s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
-                                                     s->tune.kernel);
+            cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
+                                               s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
+                                               s->tune.kernel);
+            if (s->tune.probe & 32) g.specialise = false;  // experiments: the generic row width
             // Each CTA trains its own replica of the hot rows between flushes; flushing
             // delta / n_CTA averages the replicas (local SGD + model averaging, as across
             // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every

@@ -439,17 +439,28 @@ __device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, 
 // Workers arrive on a shared-memory mbarrier once per merged center; the flusher polls
 // it (test_wait) and drains the cache whenever `flush_centers` merges have completed a
 // phase, and once more when the workers are done.
-template <int DCH, int G, int WORKERS>
+// D4 > 0 specialises the kernel for rows of exactly D4 float4 (the dims of the benchmark
+// configurations): every shared-memory and row offset becomes an immediate and the
+// last-chunk predicate a constant lane bound. D4 = 0 takes the row width at run time.
+template <int DCH, int G, int WORKERS, int D4 = 0>
 __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) {
     static_assert(G == 4, "signals are fetched as one float4 per context");
+    static_assert(D4 == 0 || (D4 > 32 * (DCH - 1) && D4 <= 32 * DCH), "D4 must belong to the variant");
     extern __shared__ float4 hsm[];
     float* sig = reinterpret_cast<float*>(hsm);
     int* codes_all = reinterpret_cast<int*>(hsm + 256);
-    float4* dblk = hsm + 256 + WORKERS * (kCodeSlots / 4);
+    // The hot-row cache and the context/prefetch rows start on 128-byte boundaries (with
+    // 32-byte rows, every staged row is then 32-byte aligned): staging at 16 mod 32 bytes
+    // made K1 ~30% slower (profiles/r1_smem_align.jsonl).
+    auto align128 = [](float4* p) {
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(p));
+        return p + ((128u - (sa & 127u)) & 127u) / 16u;
+    };
+    float4* dblk = align128(hsm + 256 + WORKERS * (kCodeSlots / 4));
     const int K = a.cache_rows;
-    const int d4 = a.d4;
+    const int d4 = D4 > 0 ? D4 : a.d4;
     int* locks = reinterpret_cast<int*>(dblk + K * d4);
-    float4* ctx_all = reinterpret_cast<float4*>(locks + ((K + 3) & ~3));
+    float4* ctx_all = align128(reinterpret_cast<float4*>(locks + ((K + 3) & ~3)));
     const int NB = a.ctx_batch;
     __shared__ int s_done;
     __shared__ uint64_t s_bar;
@@ -746,9 +757,24 @@ constexpr int kG4 = 4;
 template <int DCH>
 constexpr int kW4 = DCH == 1 ? 15 : (DCH == 2 ? 11 : 7);
 
+// Row widths with a specialised K1 (D = 100, 128, 200, 300: the benchmark configurations,
+// rows padded to 32 bytes).
+template <int DCH>
+auto hog4_for(int d4) -> decltype(&hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>) {
+    if constexpr (DCH == 1) {
+        if (d4 == 26) return hog4_kernel<1, kG4<1>, kW4<1>, 26>;
+        if (d4 == 32) return hog4_kernel<1, kG4<1>, kW4<1>, 32>;
+    } else if constexpr (DCH == 2) {
+        if (d4 == 50) return hog4_kernel<2, kG4<2>, kW4<2>, 50>;
+    } else if constexpr (DCH == 3) {
+        if (d4 == 76) return hog4_kernel<3, kG4<3>, kW4<3>, 76>;
+    }
+    return hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>;
+}
+
 template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>;
+    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : (g.specialise ? hog4_for<DCH>(a.d4) : hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>);
     if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
@@ -798,6 +824,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
                      int rows_override, int window, int kernel) {
     HogGeometry g{};
     g.kernel = kernel == 3 ? 3 : 4;
+    g.specialise = true;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -809,7 +836,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     g.blocks = blocks_override > 0 ? blocks_override : sms;
     g.cpw = std::min(cpw_override > 0 ? cpw_override : 4, 32);  // <= 32: a ticket's metadata is one lane each
     // shared memory: sigmoid table | path codes | hot-row cache (+locks) | context buffers
-    const size_t fixed = 4096 + static_cast<size_t>(workers) * kCodeSlots * 4;
+    const size_t fixed = 4096 + static_cast<size_t>(workers) * kCodeSlots * 4 + 14 * 16;
     const size_t per_row = static_cast<size_t>(d4) * 16 + 4;
     int rows = std::min(cache_rows_wanted, static_cast<int>((48 * 1024) / per_row));
     if (rows_override >= 0 && rows_override < rows) rows = rows_override;
@@ -817,8 +844,9 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     const size_t cache_bytes = static_cast<size_t>(g.cache_rows) * d4 * 16 + static_cast<size_t>((g.cache_rows + 3) & ~3) * 4;
     // v4 also stages each warp's next row group (4 rows) in shared memory. A center whose
     // 2b contexts do not fit one context batch re-reads (and re-writes) its whole path per
-    // batch, which costs more than a worker warp: unless the caller fixed the warp count,
-    // drop up to 3 warps if that lets one batch hold a full window (2W contexts).
+    // batch: unless the caller fixed the warp count, drop one warp if that lets one batch
+    // hold a full window (2W contexts). Dropping more measured slower (C4, W 10: 4 warps
+    // x batch 20 took 1577 ms, 7 warps x batch 10 1322 ms).
     const size_t budget = 225 * 1024;
     auto batch_for = [&](int warps, size_t* smem) {
         const int g4 = g.variant == 1 ? kG4<1> : (g.variant == 2 ? kG4<2> : kG4<3>);
@@ -832,7 +860,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     };
     g.ctx_batch = batch_for(g.warps, &g.smem);
     if (warps_override <= 0 && g.ctx_batch < 2 * window) {
-        for (int w = g.warps - 1; w >= std::max(1, g.warps - 3); --w) {
+        for (int w = g.warps - 1; w >= std::max(1, g.warps - 1); --w) {
             size_t sm = 0;
             const int nb = batch_for(w, &sm);
             if (nb >= 2 * window) {

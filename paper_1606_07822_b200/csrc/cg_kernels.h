@@ -128,6 +128,7 @@ struct HogGeometry {
     int ctx_batch;  // contexts staged per warp
     int variant;    // DCH
     int kernel;     // 4 = hog4_kernel (default), 3 = hog_kernel
+    bool specialise;  // v4: use the row-width-specialised instantiation when there is one
     size_t smem;
 };
 // Depth limit on cached hot rows for this row width (none for the row-major kernel).
