@@ -223,7 +223,8 @@ typedef struct cg_tuning {
                                  even K = 0 (unstable at full-GPU concurrency; experiments only) */
     int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
                                  context-row updates, bit 2 skip cache merges, bit 3 skip reading the
-                                 CTA's cached deltas; bit 5 (harmless) runs the generic-width K1
+                                 CTA's cached deltas; bit 4 (harmless) flushes the cache from the workers
+                                 even when a flusher warp fits; bit 5 (harmless) runs the generic-width K1
                                  instead of the one specialised for D = 100/128/200/300 */
     int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
 } cg_tuning;

@@ -817,6 +817,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                                                s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
                                                s->tune.kernel);
             if (s->tune.probe & 32) g.specialise = false;  // experiments: the generic row width
+            if (s->tune.probe & 16) g.flusher = false;     // experiments: workers flush inline
             // Each CTA trains its own replica of the hot rows between flushes; flushing
             // delta / n_CTA averages the replicas (local SGD + model averaging, as across
             // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every

@@ -83,7 +83,8 @@ __device__ __forceinline__ void red_add4(float* p, float4 v) {
 }
 
 // Shared-memory mbarrier used as a phase counter: workers arrive without waiting, a
-// poller tests whether a phase has completed.
+// poller tests whether a phase has completed (polling it measured cheaper than polling a
+// volatile shared counter: C5 K1 3546 vs 3660 ms).
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
     const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
@@ -103,6 +104,7 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, unsigned parity) {
         : "memory");
     return ok != 0;
 }
+
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);

@@ -436,14 +436,20 @@ __device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, 
 // each lane evaluates one sigmoid, and the updates (h_i += g U, delta += g v) follow as
 // pure FMA streams. This removes v3's serial dot -> reduce -> sigmoid -> update chain per
 // (context, group), the latency that held issue at ~46% with 12 warps per SM.
-// Workers arrive on a shared-memory mbarrier once per merged center; the flusher polls
-// it (test_wait) and drains the cache whenever `flush_centers` merges have completed a
-// phase, and once more when the workers are done.
+// Cache flushes: when the registers leave room for a warp that shared memory cannot feed
+// as a worker (C2, D 300), that warp is a dedicated flusher, polling the merge count;
+// otherwise (C1, C3: registers are the limit) the worker whose merge completes a batch
+// of `flush_centers` merged centers drains the cache itself, and its warp slot is one
+// more worker. The last worker to finish drains the cache once more. The polling
+// flusher spends ~5% of the issued instructions (__nanosleep returns almost at once;
+// sleeping in mbarrier.try_wait measured slower), but inline flushes on the workers'
+// path cost more than that where the flusher warp is free (C2 +1.7%, C5 +3.5%).
 // D4 > 0 specialises the kernel for rows of exactly D4 float4 (the dims of the benchmark
 // configurations): every shared-memory and row offset becomes an immediate and the
 // last-chunk predicate a constant lane bound. D4 = 0 takes the row width at run time.
 template <int DCH, int G, int WORKERS, int D4 = 0>
-__global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) {
+__global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
+    // WORKERS: warps per block the registers allow (workers, plus the flusher if any)
     static_assert(G == 4, "signals are fetched as one float4 per context");
     static_assert(D4 == 0 || (D4 > 32 * (DCH - 1) && D4 <= 32 * DCH), "D4 must belong to the variant");
     extern __shared__ float4 hsm[];
@@ -463,62 +469,68 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
     float4* ctx_all = align128(reinterpret_cast<float4*>(locks + ((K + 3) & ~3)));
     const int NB = a.ctx_batch;
     __shared__ int s_done;
+    __shared__ unsigned s_merged;
     __shared__ uint64_t s_bar;
     __shared__ float4 s_sig[WORKERS * 8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int workers = (blockDim.x >> 5) - 1;
+    const int workers = (blockDim.x >> 5) - a.flusher;
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
     for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
     {  // context, h and prefetch buffers: zeroed once so out-of-row reads are finite
-        const int n4 = ((blockDim.x >> 5) - 1) * (2 * NB + G) * d4;  // exactly the ctx + prefetch allocation
+        const int n4 = workers * (2 * NB + G) * d4;  // exactly the ctx + prefetch allocation
         for (int i = tid; i < n4; i += blockDim.x) ctx_all[i] = f4(0.f);
     }
     if (tid == 0) {
         s_done = 0;
+        s_merged = 0;
         mbar_init(&s_bar, static_cast<unsigned>(a.flush_centers));
     }
     __syncthreads();
 
-    if (warp == workers) {  // flusher
-        if (K == 0) return;  // nothing cached, nothing to flush
+    // Drain every cached row's delta into syn1 (whole warp): row by row under its lock,
+    // scaled per row (averaging of the CTA replicas, see cg_capi.cu), then a fence so
+    // the other SMs see the update before this CTA's next flush.
+    auto flush_cache = [&]() {
+        for (int r = 0; r < K; ++r) {
+            if (lane == 0)
+                while (atomicCAS(&locks[r], 0, 1) != 0) {
+                }
+            __syncwarp();
+            __threadfence_block();
+            float4 d[DCH];
+#pragma unroll
+            for (int k = 0; k < DCH; ++k) {
+                const int q = lane + 32 * k;
+                d[k] = f4(0.f);
+                if (in_row<DCH>(k, q, d4)) {
+                    d[k] = dblk[r * d4 + q];
+                    dblk[r * d4 + q] = f4(0.f);
+                }
+            }
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) atomicExch(&locks[r], 0);
+            const float sc = a.row_scale ? a.row_scale[r] : a.hot_flush_scale;
+#pragma unroll
+            for (int k = 0; k < DCH; ++k) {
+                const int q = lane + 32 * k;
+                if (in_row<DCH>(k, q, d4) && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
+            }
+        }
+    };
+
+    if (warp == workers) {  // flusher warp: workers arrive on s_bar once per merged center
+        if (K == 0) return;
         unsigned phase = 0;
         for (;;) {
-            // Due once flush_centers merges have completed the barrier's phase. Polled
-            // every ~20 us: sleeping in try_wait (suspend-time hint) until the phase
-            // completes measured slower (C2 K1 90.3 vs 84.7 ms, C3 156 vs 137 ms).
             __nanosleep(20000);
             const bool due = mbar_test_wait(&s_bar, phase);
             if (due) phase ^= 1u;
             const bool done = *reinterpret_cast<volatile int*>(&s_done) == workers;
             if (due || done) {
-                for (int r = 0; r < K; ++r) {
-                    if (lane == 0)
-                        while (atomicCAS(&locks[r], 0, 1) != 0) {
-                        }
-                    __syncwarp();
-                    __threadfence_block();
-                    float4 d[DCH];
-#pragma unroll
-                    for (int k = 0; k < DCH; ++k) {
-                        const int q = lane + 32 * k;
-                        d[k] = f4(0.f);
-                        if (in_row<DCH>(k, q, d4)) {
-                            d[k] = dblk[r * d4 + q];
-                            dblk[r * d4 + q] = f4(0.f);
-                        }
-                    }
-                    __threadfence_block();
-                    __syncwarp();
-                    if (lane == 0) atomicExch(&locks[r], 0);
-                    const float sc = a.row_scale ? a.row_scale[r] : a.hot_flush_scale;
-#pragma unroll
-                    for (int k = 0; k < DCH; ++k) {
-                        const int q = lane + 32 * k;
-                        if (in_row<DCH>(k, q, d4) && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
-                    }
-                }
+                flush_cache();
                 __threadfence();
             }
             if (done) break;
@@ -734,17 +746,35 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
             }
             n_pairs += static_cast<unsigned long long>(n);
             n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
-            if (lane == 0 && touched_cache) mbar_arrive(&s_bar);
+            if (touched_cache) {
+                if (a.flusher) {
+                    if (lane == 0) mbar_arrive(&s_bar);
+                } else {
+                    unsigned m = 0;
+                    if (lane == 0) m = atomicAdd(&s_merged, 1u) + 1u;
+                    m = __shfl_sync(kFull, m, 0);
+                    if (m % static_cast<unsigned>(a.flush_centers) == 0u) flush_cache();
+                }
+            }
         }
     }
+    int last = 0;
     if (lane == 0) {
         atomicAdd(a.counters + 1, n_pairs);
         atomicAdd(a.counters + 2, n_steps);
         atomicAdd(a.counters + 3, n_centers);
-        // the last worker completes the barrier's current phase so the flusher wakes for
-        // the final flush (arrivals past it only start the next, never-awaited phase)
-        if (atomicAdd(&s_done, 1) == workers - 1)
+        __threadfence_block();  // this warp's merges before its done count
+        last = atomicAdd(&s_done, 1) == workers - 1;
+        // with a flusher warp, the last worker completes the barrier's current phase so the
+        // flusher wakes for the final flush (arrivals past it start a never-awaited phase)
+        if (a.flusher && last)
             for (int i = 0; i < a.flush_centers; ++i) mbar_arrive(&s_bar);
+    }
+    // without a flusher warp, the last worker to finish drains what the others merged
+    // after their last flush
+    if (!a.flusher && __shfl_sync(kFull, last, 0) && K > 0) {
+        __threadfence_block();
+        flush_cache();
     }
 }
 
@@ -755,7 +785,7 @@ __global__ void __launch_bounds__((WORKERS + 1) * 32, 1) hog4_kernel(HogArgs a) 
 template <int DCH>
 constexpr int kG4 = 4;
 template <int DCH>
-constexpr int kW4 = DCH == 1 ? 15 : (DCH == 2 ? 11 : 7);
+constexpr int kW4 = DCH == 1 ? 16 : (DCH == 2 ? 12 : 8);
 
 // Row widths with a specialised K1 (D = 100, 128, 200, 300: the benchmark configurations,
 // rows padded to 32 bytes).
@@ -780,7 +810,8 @@ void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     b.cache_rows = g.cache_rows;
     b.centers_per_warp = g.cpw;
     b.ctx_batch = g.ctx_batch;
-    k<<<g.blocks, (g.warps + 1) * 32, g.smem, s>>>(b);
+    b.flusher = g.flusher ? 1 : 0;
+    k<<<g.blocks, (g.warps + (g.kernel == 3 || g.flusher ? 1 : 0)) * 32, g.smem, s>>>(b);  // + flusher warp
 }
 
 // Per-variant shape: float4 chunks per lane (DCH), rows trained together (G) and worker
@@ -847,7 +878,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     // batch: unless the caller fixed the warp count, drop one warp if that lets one batch
     // hold a full window (2W contexts). Dropping more measured slower (C4, W 10: 4 warps
     // x batch 20 took 1577 ms, 7 warps x batch 10 1322 ms).
-    const size_t budget = 225 * 1024;
+    const size_t budget = 227 * 1024 - 4096;  // dynamic shared memory; static (signals, counters) <= 4 KB
     auto batch_for = [&](int warps, size_t* smem) {
         const int g4 = g.variant == 1 ? kG4<1> : (g.variant == 2 ? kG4<2> : kG4<3>);
         const size_t prefetch = g.kernel == 4 ? static_cast<size_t>(warps) * g4 * d4 * 16 : 0;
@@ -871,6 +902,8 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
             }
         }
     }
+    // a warp the registers allow but shared memory cannot feed becomes the cache flusher
+    g.flusher = g.kernel == 4 && g.warps < workers && g.cache_rows > 0;
     return g;
 }
 

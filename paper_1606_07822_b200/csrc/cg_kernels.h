@@ -117,6 +117,7 @@ struct HogArgs {
     int32_t flush_centers;     // centers merged into a block cache between flushes
     int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
     int32_t ctx_batch;         // context rows staged per warp (<= 2 * window)
+    int32_t flusher;           // v4: 1 = the block's last warp is a cache flusher (set by the launcher)
     int32_t probe;             // experiments only: 1 skip cold-row updates, 2 skip syn0 updates, 4 skip cache merges
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
@@ -129,6 +130,7 @@ struct HogGeometry {
     int variant;    // DCH
     int kernel;     // 4 = hog4_kernel (default), 3 = hog_kernel
     bool specialise;  // v4: use the row-width-specialised instantiation when there is one
+    bool flusher;     // v4: one extra (flusher) warp; only when registers leave room for it
     size_t smem;
 };
 // Depth limit on cached hot rows for this row width (none for the row-major kernel).
