@@ -118,3 +118,30 @@ def test_hogwild_planted_cluster_recall_matches_reference():
     r_gpu = recall_at_10(m.syn0, cluster, sample)
     assert r_ref > 0.3
     assert abs(r_gpu - r_ref) <= 0.02, (r_gpu, r_ref)
+
+
+# Every K1 instantiation: the row-width-specialised ones (D 100/128/200/300) and the
+# generic ones of each float4-chunk count (D 16/180/260), with the flusher warp (C2/C5
+# geometry) and with inline flushes (probe bit 4). Each must cover the stream and learn:
+# at least 90% of the loss reduction of the reference's own single-stream training on
+# the same corpus (the deterministic path, which is bit-identical to the reference).
+@pytest.mark.parametrize("dim,window,probe", [(100, 5, 0), (128, 5, 0), (200, 5, 0), (300, 5, 0), (300, 10, 0),
+                                              (16, 5, 0), (180, 5, 0), (260, 5, 0), (200, 5, 16), (200, 5, 32),
+                                              (300, 5, 48)])
+def test_hogwild_every_kernel_variant_learns(dim, window, probe):
+    c = CorpusConfig("variants", 300_000, 5000, 1.0, dim, window, 1e-3, 1, 11)
+    vocab, ids = vocab_from_raw(generate(c), 1, c.vocab)
+    tree, sel = setup(vocab)
+    base = dict(dim=dim, window=window, min_count=1, sample=c.sample, iterations=1, cache_nodes=31, seed=11)
+    det = api.train(ids, vocab, tree, sel, api.TrainConfig(**base, mode="deterministic"))
+    s = api.Session(vocab, tree, sel, api.TrainConfig(**base, mode="hogwild"))
+    s.tune(probe=probe)
+    s.upload_ids(ids)
+    e = s.train_range(0, 0, ids.size, 0, 1)
+    m = s.download()
+    s.close()
+    assert e.words == ids.size and e.pairs > 0
+    assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
+    init = api.init_model(vocab.size(), dim, 11)
+    li, ld, lh = (_loss(x, tree, vocab, ids, c) for x in (init, det, m))
+    assert li - lh > 0.9 * (li - ld), (lh, ld, li, e.worker_warps, e.ctx_batch, e.cached_rows)
