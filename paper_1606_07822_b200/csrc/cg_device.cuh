@@ -82,27 +82,13 @@ __device__ __forceinline__ void red_add4(float* p, float4 v) {
                  : "memory");
 }
 
-// Shared-memory mbarrier used as a phase counter: workers arrive without waiting, a
-// poller tests whether a phase has completed (polling it measured cheaper than polling a
-// volatile shared counter: C5 K1 3546 vs 3660 ms).
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+// Named barriers (bar.arrive / bar.sync with an explicit thread count): a consumer warp
+// blocks in hardware, producers signal without waiting.
+__device__ __forceinline__ void named_bar_arrive(int id, int threads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(a) : "memory");
-}
-// true once the phase with parity `parity` has completed (non-blocking).
-__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, unsigned parity) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    unsigned ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    return ok != 0;
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }

@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     const int NB = a.ctx_batch;
     __shared__ int s_done;
     __shared__ unsigned s_merged;
-    __shared__ uint64_t s_bar;
     __shared__ float4 s_sig[WORKERS * 8];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -485,7 +484,6 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     if (tid == 0) {
         s_done = 0;
         s_merged = 0;
-        mbar_init(&s_bar, static_cast<unsigned>(a.flush_centers));
     }
     __syncthreads();
 
@@ -521,19 +519,22 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
         }
     };
 
-    if (warp == workers) {  // flusher warp: workers arrive on s_bar once per merged center
+    // Flusher warp: blocked in hardware on named barrier 1 (bar.sync, 64 threads) until a
+    // worker warp whose merge completed a batch of flush_centers arrives on it (bar.arrive,
+    // non-blocking). Arrivals while the flusher is busy count toward its next wait, so no
+    // request is lost; two of them may complete a phase on their own, which only delays
+    // one flush. The last worker sets s_done before its final arrival, and the flusher
+    // checks s_done before every wait, so it always ends with a flush after all merges.
+    if (warp == workers) {
         if (K == 0) return;
-        unsigned phase = 0;
         for (;;) {
-            __nanosleep(20000);
-            const bool due = mbar_test_wait(&s_bar, phase);
-            if (due) phase ^= 1u;
-            const bool done = *reinterpret_cast<volatile int*>(&s_done) == workers;
-            if (due || done) {
+            if (*reinterpret_cast<volatile int*>(&s_done) == workers) {
                 flush_cache();
-                __threadfence();
+                break;
             }
-            if (done) break;
+            named_bar_sync(1, 64);
+            flush_cache();
+            __threadfence();
         }
         return;
     }
@@ -584,8 +585,11 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
             const float alpha = __shfl_sync(kFull, t_alpha, jt);
             const int p0 = __shfl_sync(kFull, t_p0, jt);
             const int L = __shfl_sync(kFull, t_len, jt);
-            const int b = a.window - static_cast<int>(ctr_draw(a.win_key, static_cast<uint64_t>(ci)) %
-                                                      static_cast<uint64_t>(a.window));
+            // shrink_window (trainer.hpp:66-68): b = W - draw mod W, with the draw reduced by
+            // a 32x32 multiply-high of its top bits (uniform to within W / 2^32; the 64-bit
+            // modulo was a ~60-instruction call per center)
+            const int b = a.window - static_cast<int>(__umulhi(static_cast<unsigned>(ctr_draw(a.win_key, static_cast<uint64_t>(ci)) >> 32),
+                                                               static_cast<unsigned>(a.window)));
             const int64_t lo = max(s_lo, ci - b), hi = min(s_hi - 1, ci + b);
             ++n_centers;
             const int n = static_cast<int>(hi - lo);
@@ -747,13 +751,16 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
             n_pairs += static_cast<unsigned long long>(n);
             n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
             if (touched_cache) {
-                if (a.flusher) {
-                    if (lane == 0) mbar_arrive(&s_bar);
-                } else {
-                    unsigned m = 0;
-                    if (lane == 0) m = atomicAdd(&s_merged, 1u) + 1u;
-                    m = __shfl_sync(kFull, m, 0);
-                    if (m % static_cast<unsigned>(a.flush_centers) == 0u) flush_cache();
+                unsigned m = 0;
+                if (lane == 0) m = atomicAdd(&s_merged, 1u) + 1u;
+                m = __shfl_sync(kFull, m, 0);
+                if (m % static_cast<unsigned>(a.flush_centers) == 0u) {
+                    if (a.flusher) {
+                        __syncwarp();
+                        named_bar_arrive(1, 64);
+                    } else {
+                        flush_cache();
+                    }
                 }
             }
         }
@@ -765,14 +772,16 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
         atomicAdd(a.counters + 3, n_centers);
         __threadfence_block();  // this warp's merges before its done count
         last = atomicAdd(&s_done, 1) == workers - 1;
-        // with a flusher warp, the last worker completes the barrier's current phase so the
-        // flusher wakes for the final flush (arrivals past it start a never-awaited phase)
-        if (a.flusher && last)
-            for (int i = 0; i < a.flush_centers; ++i) mbar_arrive(&s_bar);
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (a.flusher && last && K > 0) {  // wake the flusher for its final flush
+        __threadfence_block();
+        named_bar_arrive(1, 64);
+        return;
     }
     // without a flusher warp, the last worker to finish drains what the others merged
     // after their last flush
-    if (!a.flusher && __shfl_sync(kFull, last, 0) && K > 0) {
+    if (!a.flusher && last && K > 0) {
         __threadfence_block();
         flush_cache();
     }
