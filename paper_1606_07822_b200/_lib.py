@@ -13,7 +13,9 @@ from pathlib import Path
 import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "libcachegram_b200.so"
+# CG_LIB: an alternative build of the same library (tools/ab_build.py, same-box A/B
+# timing of kernel variants); unset in every test, smoke and bench run.
+LIB_PATH = Path(os.environ["CG_LIB"]) if os.environ.get("CG_LIB") else PKG_DIR / "libcachegram_b200.so"
 
 CG_OK = 0
 CG_ERR_INVALID_ARGUMENT = 1

@@ -31,6 +31,10 @@
 #include "cg_device.cuh"
 #include "cg_kernels.h"
 
+#ifndef CG_EXP
+#define CG_EXP 0  // kernel experiments (tools/ab_build.py); 0 in every shipped build
+#endif
+
 namespace cgk {
 namespace {
 
@@ -409,10 +413,22 @@ __device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, 
         for (int k = 0; k < DCH; ++k) v[k] = V[i * d4 + lane + 32 * k];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
+            if constexpr (CG_EXP == 4) {  // experiment: two partial sums per dot
+                float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                for (int k = 0; k < DCH; ++k) {
+                    a0 = fmaf(v[k].x, U[g][k].x, a0);
+                    a1 = fmaf(v[k].y, U[g][k].y, a1);
+                    a0 = fmaf(v[k].z, U[g][k].z, a0);
+                    a1 = fmaf(v[k].w, U[g][k].w, a1);
+                }
+                p[ii * G + g] = a0 + a1;
+            } else {
             float acc = 0.f;
 #pragma unroll
             for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
             p[ii * G + g] = acc;
+            }
         }
     }
     const float tot = transpose_reduce<N>(p, lane);
@@ -675,6 +691,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                         // Lanes past the row end compute on neighbouring data; their hacc
                         // and delta chunks are never written back.
                         const int ni = min(cic, r);
+                        if constexpr (DCH < 3 && CG_EXP != 3) {
 #pragma unroll 1
                         for (int ii = 0; ii < ni; ++ii) {
                             const int i = cc + ii;
@@ -686,9 +703,19 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                                 v[k] = V[i * d4 + lane + 32 * k];
                                 hacc[k] = Hs[i * d4 + lane + 32 * k];
                             }
-                            const float4 g4 = reinterpret_cast<const float4*>(sg)[ii];
                             // one broadcast load instead of G shuffles: C2 K1 92.2 -> 90.3 ms
+                            const float4 g4 = reinterpret_cast<const float4*>(sg)[ii];
                             const float gg[G] = {g4.x, g4.y, g4.z, g4.w};
+                            if constexpr (CG_EXP == 1) {  // experiment: Dl FMAs first
+#pragma unroll
+                                for (int g = 0; g < G; ++g)
+#pragma unroll
+                                    for (int k = 0; k < DCH; ++k) Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
+#pragma unroll
+                                for (int g = 0; g < G; ++g)
+#pragma unroll
+                                    for (int k = 0; k < DCH; ++k) hacc[k] = axpy4(gg[g], U[g][k], hacc[k]);
+                            } else {
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -697,11 +724,53 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                                     Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
                                 }
                             }
+                            }
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
                                 if (in_row<DCH>(k, q, d4)) Hs[i * d4 + q] = hacc[k];
                             }
+                        }
+                        } else {
+                        const float4* sg4 = reinterpret_cast<const float4*>(sg);
+                        // D > 256: software-pipelined. The next context's v and signals
+                        // are loaded while this one's FMAs run, and the Dl FMAs go first so
+                        // the h row loaded at the top arrives before its FMAs (C4 1287 ->
+                        // 1241 ms; at D <= 256 it measured slower: C2 72.8 -> 75.6 ms).
+                        float4 vn[DCH];
+#pragma unroll
+                        for (int k = 0; k < DCH; ++k) vn[k] = V[cc * d4 + lane + 32 * k];
+                        float4 gn = sg4[0];
+#pragma unroll 1
+                        for (int ii = 0; ii < ni; ++ii) {
+                            const int i = cc + ii;
+                            float4 v[DCH], hacc[DCH];
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                v[k] = vn[k];
+                                hacc[k] = Hs[i * d4 + lane + 32 * k];
+                            }
+                            const float gg[G] = {gn.x, gn.y, gn.z, gn.w};
+                            const int in = min(ii + 1, ni - 1);
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) vn[k] = V[(cc + in) * d4 + lane + 32 * k];
+                            gn = sg4[in];
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+#pragma unroll
+                                for (int k = 0; k < DCH; ++k) Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
+                            }
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+#pragma unroll
+                                for (int k = 0; k < DCH; ++k) hacc[k] = axpy4(gg[g], U[g][k], hacc[k]);
+                            }
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (in_row<DCH>(k, q, d4)) Hs[i * d4 + q] = hacc[k];
+                            }
+                        }
                         }
                         cc += cic;
                     }
