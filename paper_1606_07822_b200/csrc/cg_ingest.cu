@@ -304,7 +304,9 @@ unsigned grid_of(uint64_t n) { return static_cast<unsigned>(std::min<uint64_t>((
 // separator (or at EOF) so that no token straddles two chunks.
 class ChunkReader {
 public:
-    ChunkReader(const char* path, size_t chunk) : cap_(chunk) {
+    // first > 0: the first chunk holds at most `first` bytes and each next one twice the
+    // previous, up to `chunk` (a consumer that starts on the first chunk waits less)
+    ChunkReader(const char* path, size_t chunk, size_t first = 0) : cap_(chunk), limit_(first ? std::min(first, chunk) : chunk) {
         f_ = std::fopen(path, "rb");
         if (!f_) throw cachegram::IoError(std::string("cannot open corpus file: ") + path);
         for (auto& b : buf_) b = static_cast<unsigned char*>(cgint::PinnedPool::get().alloc(cap_));
@@ -319,9 +321,11 @@ public:
         size_t have = carry_.size();
         if (have) std::memcpy(b, carry_.data(), have);
         carry_.clear();
-        if (!eof_ && have < cap_) {
-            const size_t got = parallel_read(b + have, cap_ - have);
-            if (got < cap_ - have) eof_ = true;
+        const size_t lim = std::max(std::min(cap_, limit_), have);
+        limit_ = std::min(cap_, limit_ * 2);
+        if (!eof_ && have < lim) {
+            const size_t got = parallel_read(b + have, lim - have);
+            if (got < lim - have) eof_ = true;
             have += got;
         }
         if (eof_ || have == 0) return have;
@@ -393,6 +397,7 @@ private:
 
     std::FILE* f_ = nullptr;
     size_t cap_;
+    size_t limit_;
     unsigned char* buf_[2] = {nullptr, nullptr};
     std::vector<unsigned char> carry_;
     bool eof_ = false;
@@ -442,7 +447,8 @@ int64_t ingest_ids(const char* path, const WordTableDev& table, int32_t* out, ui
                    IngestStats* stats, const IngestProgress* progress) {
     const auto t0 = std::chrono::steady_clock::now();
     // small enough that reading overlaps tokenising (CG_INGEST_CHUNK overrides, for tests)
-    ChunkReader rd(path, chunk_bytes(size_t{32} << 20));
+    // (the first chunks ramp up from 4 MB, so training on them starts sooner)
+    ChunkReader rd(path, chunk_bytes(size_t{32} << 20), progress ? chunk_bytes(size_t{4} << 20) : 0);
     unsigned char* dbytes[2] = {nullptr, nullptr};
     int32_t* tmp = nullptr;
     uint32_t* tcount = nullptr;
