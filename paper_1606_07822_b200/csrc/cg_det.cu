@@ -303,13 +303,13 @@ size_t det_smem_bytes(int D) { return (1024 + 2 * static_cast<size_t>(D) + 32 + 
 
 void launch_det_pass(const DetModel& m, const DetPass& p, DetState* state, cudaStream_t s) {
     const size_t smem = det_smem_bytes(m.dim);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(det_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(det_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));  // static + dynamic may pass 48 KB
     det_pass_kernel<<<1, 32, smem, s>>>(m, p, state);
 }
 
 void launch_det_center(const DetModel& m, const DetCenter& c, cudaStream_t s) {
     const size_t smem = det_smem_bytes(m.dim);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(det_center_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(det_center_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));  // static + dynamic may pass 48 KB
     det_center_kernel<<<1, 32, smem, s>>>(m, c);
 }
 
@@ -318,7 +318,7 @@ void launch_det_flush_flags(const DetModel& m, cudaStream_t s) { det_flush_flags
 void launch_det_pair(const DetModel& m, int32_t center, int32_t context, float alpha, int phase, float* buf,
                      int32_t* n_acquired, cudaStream_t s) {
     const size_t smem = det_smem_bytes(m.dim);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(det_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(det_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));  // static + dynamic may pass 48 KB
     det_pair_kernel<<<1, 32, smem, s>>>(m, center, context, alpha, phase, buf, n_acquired);
 }
 

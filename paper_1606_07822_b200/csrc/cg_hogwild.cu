@@ -883,7 +883,9 @@ auto hog4_for(int d4) -> decltype(&hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>) {
 template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : (g.specialise ? hog4_for<DCH>(a.d4) : hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>);
-    if (g.smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
+    // always opt in: dynamic + static shared memory above 48 KB needs it even when the
+    // dynamic part alone is below (a launch without it failed with "invalid argument")
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     HogArgs b = a;
     b.cache_rows = g.cache_rows;
     b.centers_per_warp = g.cpw;
