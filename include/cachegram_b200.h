@@ -211,7 +211,7 @@ CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* byt
 typedef struct cg_tuning {
     int32_t blocks;           /* 0 = one persistent CTA per SM */
     int32_t warps_per_block;  /* 0 = the variant's maximum */
-    int32_t centers_per_warp; /* 0 = 8: centers a warp trains between block-cache flushes */
+    int32_t centers_per_warp; /* 0 = auto: consecutive kept centers per work ticket (16, or 8 for small passes) */
     int32_t smem_cache_rows;  /* < 0 = min(K, what fits); hot rows held in the block cache */
     int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
     float hot_flush_scale;    /* 0 = per-row 1/E[#CTAs contributing per flush] (averaging of overlapping

@@ -815,7 +815,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.probe = s->tune.probe;
             cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
                                                s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
-                                               s->tune.kernel);
+                                               s->tune.kernel, n);
             if (s->tune.probe & 32) g.specialise = false;  // experiments: the generic row width
             if (s->tune.probe & 16) g.flusher = false;     // experiments: workers flush inline
             // Each CTA trains its own replica of the hot rows between flushes; flushing

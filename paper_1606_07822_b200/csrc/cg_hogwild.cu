@@ -31,9 +31,6 @@
 #include "cg_device.cuh"
 #include "cg_kernels.h"
 
-#ifndef CG_EXP
-#define CG_EXP 0  // kernel experiments (tools/ab_build.py); 0 in every shipped build
-#endif
 
 namespace cgk {
 namespace {
@@ -413,22 +410,10 @@ __device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, 
         for (int k = 0; k < DCH; ++k) v[k] = V[i * d4 + lane + 32 * k];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-            if constexpr (CG_EXP == 4) {  // experiment: two partial sums per dot
-                float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    a0 = fmaf(v[k].x, U[g][k].x, a0);
-                    a1 = fmaf(v[k].y, U[g][k].y, a1);
-                    a0 = fmaf(v[k].z, U[g][k].z, a0);
-                    a1 = fmaf(v[k].w, U[g][k].w, a1);
-                }
-                p[ii * G + g] = a0 + a1;
-            } else {
             float acc = 0.f;
 #pragma unroll
             for (int k = 0; k < DCH; ++k) acc = dot4(v[k], U[g][k], acc);
             p[ii * G + g] = acc;
-            }
         }
     }
     const float tot = transpose_reduce<N>(p, lane);
@@ -691,7 +676,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                         // Lanes past the row end compute on neighbouring data; their hacc
                         // and delta chunks are never written back.
                         const int ni = min(cic, r);
-                        if constexpr (DCH < 3 && CG_EXP != 3) {
+                        if constexpr (DCH < 3) {
 #pragma unroll 1
                         for (int ii = 0; ii < ni; ++ii) {
                             const int i = cc + ii;
@@ -706,16 +691,6 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                             // one broadcast load instead of G shuffles: C2 K1 92.2 -> 90.3 ms
                             const float4 g4 = reinterpret_cast<const float4*>(sg)[ii];
                             const float gg[G] = {g4.x, g4.y, g4.z, g4.w};
-                            if constexpr (CG_EXP == 1) {  // experiment: Dl FMAs first
-#pragma unroll
-                                for (int g = 0; g < G; ++g)
-#pragma unroll
-                                    for (int k = 0; k < DCH; ++k) Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
-#pragma unroll
-                                for (int g = 0; g < G; ++g)
-#pragma unroll
-                                    for (int k = 0; k < DCH; ++k) hacc[k] = axpy4(gg[g], U[g][k], hacc[k]);
-                            } else {
 #pragma unroll
                             for (int g = 0; g < G; ++g) {
 #pragma unroll
@@ -723,7 +698,6 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                                     hacc[k] = axpy4(gg[g], U[g][k], hacc[k]);
                                     Dl[g][k] = axpy4(gg[g], v[k], Dl[g][k]);
                                 }
-                            }
                             }
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
@@ -932,7 +906,7 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
 int hog_hmax(int) { return 1 << 30; }
 
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window, int kernel) {
+                     int rows_override, int window, int kernel, int64_t tokens) {
     HogGeometry g{};
     g.kernel = kernel == 3 ? 3 : 4;
     g.specialise = true;
@@ -982,6 +956,10 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
             }
         }
     }
+    // Centers per ticket: 16 when every warp gets >= 2000 tokens (fewer ticket atomics and
+    // metadata loads: C2 -1%, C3 -1.2%, C5 -1.4% vs 4), else 8 (the tail of a small pass
+    // grows with the ticket: C1 3.33 ms at 8, 3.44 at 32).
+    if (cpw_override <= 0) g.cpw = tokens / (static_cast<int64_t>(g.blocks) * g.warps) >= 2000 ? 16 : 8;
     // a warp the registers allow but shared memory cannot feed becomes the cache flusher
     g.flusher = g.kernel == 4 && g.warps < workers && g.cache_rows > 0;
     return g;

@@ -137,7 +137,7 @@ struct HogGeometry {
 int hog_hmax(int d4);
 // Picks the kernel variant for d4 and the launch geometry for the device.
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window, int kernel);
+                     int rows_override, int window, int kernel, int64_t tokens);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 // ---------------- evaluation (cg_eval.cu) -----------------------------------------
