@@ -169,3 +169,30 @@ def test_hogwild_train_from_file_pipelined(tmp_path, monkeypatch):
     m2 = api.train(path, small, tree2, api.select_cached_nodes(tree2, 31), tc, st2)
     assert st2.words_processed == 2 * ids_small.size
     assert np.isfinite(m2.syn0).all()
+
+
+def test_hogwild_train_from_file_ramped_chunks(tmp_path):
+    """Without the chunk override the pipelined reader ramps its chunks up from 4 MB
+    (4, 8, 16, 32 MB ...): a ~14 MB file is trained in several launches while it is
+    read, covering every token once, with the same id stream as the host reader."""
+    rng = np.random.default_rng(21)
+    words = np.array([f"w{i}" for i in range(20000)])
+    path = str(tmp_path / "r.txt")
+    with open(path, "w") as f:
+        for _ in range(7):
+            f.write(" ".join(words[np.minimum(rng.zipf(1.1, 400_000), 20000) - 1]) + "\n")
+    assert Path(path).stat().st_size > 12 << 20
+    vocab = api.build_vocabulary_file(path, 1)
+    ids = api.read_id_stream(path, vocab)
+    tree = api.build_huffman_tree(vocab)
+    sel = api.select_cached_nodes(tree, 31)
+    tc = api.TrainConfig(dim=16, window=5, min_count=1, sample=1e-3, iterations=1, cache_nodes=31, seed=5,
+                         mode="hogwild")
+    st = api.TrainStats()
+    m = api.train(path, vocab, tree, sel, tc, st)
+    assert st.words_processed == ids.size
+    assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
+    t = O.Tree(tree.offsets, tree.nodes, tree.turns, tree.usage)
+    cen, ctx = O.sample_pairs(ids, vocab.counts, vocab.total_tokens(), 1e-3, 5, 7, 1 << 15)
+    init = api.init_model(vocab.size(), 16, 5)
+    assert O.hs_loss(cen, ctx, m.syn0, m.syn1, t) < O.hs_loss(cen, ctx, init.syn0, init.syn1, t)
