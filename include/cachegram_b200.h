@@ -225,7 +225,8 @@ typedef struct cg_tuning {
                                  context-row updates, bit 2 skip cache merges, bit 3 skip reading the
                                  CTA's cached deltas; bit 4 (harmless) flushes the cache from the workers
                                  even when a flusher warp fits; bit 5 (harmless) runs the generic-width K1
-                                 instead of the one specialised for D = 100/128/200/300 */
+                                 instead of the one specialised for D = 100/128/200/300; bit 6 does not
+                                 cache the most frequent words' syn0 rows (unstable without subsampling) */
     int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);

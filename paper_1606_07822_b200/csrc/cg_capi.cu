@@ -209,6 +209,7 @@ struct cg_session {
     cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0, 0, 0};
     int32_t cached_rows = 0;  // hogwild: rows [0, cached_rows) of syn1 are eligible for the CTA cache
     std::vector<double> row_share;  // hogwild: usage share (of the root's) of the cache-eligible rows
+    std::vector<double> ctx_share;  // hogwild: share of centers with word w (w < kCtxCacheRows) in their window
     DevBuf<float> row_scale;
     int scale_blocks = -1, scale_flush = -1, scale_rows = -1;
 
@@ -521,6 +522,18 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                     static_cast<float>(cachegram::keep_probability(md->counts[w], md->total_tokens, cfg->sample));
             s->keep.upload(kp.data(), kp.size(), s->stream);
         }
+        {  // expected share of centers whose window holds word w, for the most frequent words:
+           // (W + 1) x its share of the kept stream (b is uniform on 1..W: E[2b] = W + 1)
+            double kept_total = 0.0;
+            std::vector<double> kept(static_cast<size_t>(std::min<int32_t>(V, cgk::kCtxCacheRows)));
+            for (int32_t w = 0; w < V; ++w) {
+                const double kpw = cfg->sample > 0.0 ? std::min(1.0, cachegram::keep_probability(md->counts[w], md->total_tokens, cfg->sample)) : 1.0;
+                const double k = static_cast<double>(md->counts[w]) * kpw;
+                kept_total += k;
+                if (w < static_cast<int32_t>(kept.size())) kept[static_cast<size_t>(w)] = k;
+            }
+            for (double k : kept) s->ctx_share.push_back(std::min(1.0, (cfg->window + 1) * k / std::max(kept_total, 1.0)));
+        }
 
         if (mode == CG_MODE_DETERMINISTIC) {
             s->model.alloc(static_cast<size_t>(V) * s->D + static_cast<size_t>(V - 1) * s->D);
@@ -810,12 +823,28 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             constexpr int32_t kGpuCacheRows = 8;
             const int32_t want_rows =
                 s->tune.min_cache_rows < 0 ? s->K : std::min(s->cached_rows, std::max(kGpuCacheRows, s->tune.min_cache_rows));
+            // The most frequent words' syn0 rows are cached too when their expected number of
+            // concurrent updaters -- the share of centers with the word in their window x the
+            // warps training at once -- reaches kHotUpdaters. Without subsampling (sample 0)
+            // the top words of C1/C2 reach ~1400 and summed stale updates diverged; cached
+            // and averaged, the loss matches the reference's (6.6130 vs 6.6128 at C1). With
+            // subsampling no word of C1-C5 gets there, and averaging would slow their learning.
+            constexpr double kHotUpdaters = 256.0;
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+            const double inflight = static_cast<double>(s->tune.blocks > 0 ? s->tune.blocks : sms) *
+                                    cgk::hog_max_warps(s->Dp / 4);
+            int32_t ctx_rows = 0;
+            while (ctx_rows < static_cast<int32_t>(s->ctx_share.size()) &&
+                   s->ctx_share[static_cast<size_t>(ctx_rows)] * inflight >= kHotUpdaters)
+                ++ctx_rows;
+            if (s->tune.probe & 64) ctx_rows = 0;
             h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 128;  // 32: +22% K1 time at C2, 64: +8%, 256: same as 128 (profiles/r1_perf4_c2.jsonl)
             h.dummy_row = s->V - 1;
             h.probe = s->tune.probe;
             cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
                                                s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
-                                               s->tune.kernel, n);
+                                               s->tune.kernel, n, ctx_rows);
             if (s->tune.probe & 32) g.specialise = false;  // experiments: the generic row width
             if (s->tune.probe & 16) g.flusher = false;     // experiments: workers flush inline
             // Each CTA trains its own replica of the hot rows between flushes; flushing
@@ -828,18 +857,25 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // merged centers with probability 1 - (1 - q)^F; averaging over that many
             // replicas keeps the hot rows stable while deep cached rows still sum.
             h.row_scale = nullptr;
-            if (s->tune.hot_flush_scale <= 0.0f && !s->row_share.empty() && g.cache_rows > 0) {
-                if (s->scale_blocks != g.blocks || s->scale_flush != h.flush_centers || s->scale_rows != g.cache_rows) {
-                    std::vector<float> sc(static_cast<size_t>(g.cache_rows));
-                    for (int32_t r = 0; r < g.cache_rows; ++r) {
-                        const double q = r < static_cast<int32_t>(s->row_share.size()) ? s->row_share[static_cast<size_t>(r)] : 0.0;
+            h.ctx_cache_rows = g.ctx_rows;
+            if (s->tune.hot_flush_scale <= 0.0f && (g.cache_rows > 0 || g.ctx_rows > 0)) {
+                if (s->scale_blocks != g.blocks || s->scale_flush != h.flush_centers || s->scale_rows != g.cache_rows * 4096 + g.ctx_rows) {
+                    // syn1 cached rows [0, cache_rows), then the cached syn0 rows [0, ctx_rows)
+                    std::vector<float> sc(static_cast<size_t>(g.cache_rows + g.ctx_rows));
+                    auto scale_of = [&](double q) {
                         const double p = 1.0 - std::pow(1.0 - std::min(q, 1.0), static_cast<double>(h.flush_centers));
-                        sc[static_cast<size_t>(r)] = static_cast<float>(1.0 / std::max(1.0, p * g.blocks));
-                    }
+                        return static_cast<float>(1.0 / std::max(1.0, p * g.blocks));
+                    };
+                    for (int32_t r = 0; r < g.cache_rows; ++r)
+                        sc[static_cast<size_t>(r)] =
+                            scale_of(r < static_cast<int32_t>(s->row_share.size()) ? s->row_share[static_cast<size_t>(r)] : 0.0);
+                    for (int32_t r = 0; r < g.ctx_rows; ++r)
+                        sc[static_cast<size_t>(g.cache_rows + r)] =
+                            scale_of(r < static_cast<int32_t>(s->ctx_share.size()) ? s->ctx_share[static_cast<size_t>(r)] : 0.0);
                     s->row_scale.upload(sc.data(), sc.size(), s->stream);
                     s->scale_blocks = g.blocks;
                     s->scale_flush = h.flush_centers;
-                    s->scale_rows = g.cache_rows;
+                    s->scale_rows = g.cache_rows * 4096 + g.ctx_rows;
                 }
                 h.row_scale = s->row_scale.p;
             }

@@ -448,7 +448,10 @@ __device__ __forceinline__ void chunk_signal(const float4* V, int d4, int lane, 
 // D4 > 0 specialises the kernel for rows of exactly D4 float4 (the dims of the benchmark
 // configurations): every shared-memory and row offset becomes an immediate and the
 // last-chunk predicate a constant lane bound. D4 = 0 takes the row width at run time.
-template <int DCH, int G, int WORKERS, int D4 = 0>
+// CTX: the most frequent words' syn0 rows are cached per CTA too (only instantiated into
+// the launch when some word's expected concurrent updaters pass the threshold in
+// cg_capi.cu; the code is compiled out otherwise, where it measured 3-4% slower).
+template <int DCH, int G, int WORKERS, int D4 = 0, bool CTX = false>
 __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     // WORKERS: warps per block the registers allow (workers, plus the flusher if any)
     static_assert(G == 4, "signals are fetched as one float4 per context");
@@ -467,7 +470,11 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     const int K = a.cache_rows;
     const int d4 = D4 > 0 ? D4 : a.d4;
     int* locks = reinterpret_cast<int*>(dblk + K * d4);
-    float4* ctx_all = align128(reinterpret_cast<float4*>(locks + ((K + 3) & ~3)));
+    // the CTA's pending deltas of the most frequent words' syn0 rows (context rows)
+    const int K0 = CTX ? a.ctx_cache_rows : 0;
+    float4* dblk0 = align128(reinterpret_cast<float4*>(locks + ((K + 3) & ~3)));
+    int* locks0 = reinterpret_cast<int*>(dblk0 + K0 * d4);
+    float4* ctx_all = align128(reinterpret_cast<float4*>(locks0 + ((K0 + 3) & ~3)));
     const int NB = a.ctx_batch;
     __shared__ int s_done;
     __shared__ unsigned s_merged;
@@ -478,6 +485,8 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < K * d4; i += blockDim.x) dblk[i] = f4(0.f);
     for (int i = tid; i < K; i += blockDim.x) locks[i] = 0;
+    for (int i = tid; i < K0 * d4; i += blockDim.x) dblk0[i] = f4(0.f);
+    for (int i = tid; i < K0; i += blockDim.x) locks0[i] = 0;
     {  // context, h and prefetch buffers: zeroed once so out-of-row reads are finite
         const int n4 = workers * (2 * NB + G) * d4;  // exactly the ctx + prefetch allocation
         for (int i = tid; i < n4; i += blockDim.x) ctx_all[i] = f4(0.f);
@@ -491,10 +500,10 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     // Drain every cached row's delta into syn1 (whole warp): row by row under its lock,
     // scaled per row (averaging of the CTA replicas, see cg_capi.cu), then a fence so
     // the other SMs see the update before this CTA's next flush.
-    auto flush_cache = [&]() {
-        for (int r = 0; r < K; ++r) {
+    auto drain_rows = [&](float4* cache, int* lk, int n, float* dst, int scale_base) {
+        for (int r = 0; r < n; ++r) {
             if (lane == 0)
-                while (atomicCAS(&locks[r], 0, 1) != 0) {
+                while (atomicCAS(&lk[r], 0, 1) != 0) {
                 }
             __syncwarp();
             __threadfence_block();
@@ -504,20 +513,24 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                 const int q = lane + 32 * k;
                 d[k] = f4(0.f);
                 if (in_row<DCH>(k, q, d4)) {
-                    d[k] = dblk[r * d4 + q];
-                    dblk[r * d4 + q] = f4(0.f);
+                    d[k] = cache[r * d4 + q];
+                    cache[r * d4 + q] = f4(0.f);
                 }
             }
             __threadfence_block();
             __syncwarp();
-            if (lane == 0) atomicExch(&locks[r], 0);
-            const float sc = a.row_scale ? a.row_scale[r] : a.hot_flush_scale;
+            if (lane == 0) atomicExch(&lk[r], 0);
+            const float sc = a.row_scale ? a.row_scale[scale_base + r] : a.hot_flush_scale;
 #pragma unroll
             for (int k = 0; k < DCH; ++k) {
                 const int q = lane + 32 * k;
-                if (in_row<DCH>(k, q, d4) && nonzero4(d[k])) red_add4(a.syn1 + 4 * (r * d4 + q), scale4(sc, d[k]));
+                if (in_row<DCH>(k, q, d4) && nonzero4(d[k])) red_add4(dst + 4 * (r * d4 + q), scale4(sc, d[k]));
             }
         }
+    };
+    auto flush_cache = [&]() {
+        drain_rows(dblk, locks, K, a.syn1, 0);
+        if constexpr (CTX) drain_rows(dblk0, locks0, K0, a.syn0, K);
     };
 
     // Flusher warp: blocked in hardware on named barrier 1 (bar.sync, 64 threads) until a
@@ -527,7 +540,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
     // one flush. The last worker sets s_done before its final arrival, and the flusher
     // checks s_done before every wait, so it always ends with a flush after all merges.
     if (warp == workers) {
-        if (K == 0) return;
+        if (K == 0 && K0 == 0) return;
         for (;;) {
             if (*reinterpret_cast<volatile int*>(&s_done) == workers) {
                 flush_cache();
@@ -609,6 +622,9 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                     pos += pos >= ci;  // skip the center's own position
                     xid = a.kept[pos];
                 }
+                // contexts whose syn0 row is in the CTA cache (word ids are in count order)
+                unsigned hot_ctx = 0;
+                if constexpr (CTX) hot_ctx = __ballot_sync(kFull, lane < nb && xid < K0);
                 __syncwarp();  // codes visible; Ub free
                 prefetch_group(0);
                 for (int i = 0; i < nb; ++i) {
@@ -625,6 +641,18 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                 for (int j0 = 0; j0 < L; j0 += G) {
                     cp_async_wait_all();  // this group's rows (and, first time, the contexts)
                     __syncwarp();
+                    if (CTX && j0 == 0 && hot_ctx) {  // + this CTA's cached delta of hot context rows
+                        for (unsigned m = hot_ctx; m; m &= m - 1) {
+                            const int i = __ffs(m) - 1;
+                            const int x = __shfl_sync(kFull, xid, i);
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (in_row<DCH>(k, q, d4)) V[i * d4 + q] = add4(V[i * d4 + q], dblk0[x * d4 + q]);
+                            }
+                        }
+                        __syncwarp();
+                    }
                     float4 U[G][DCH], Dl[G][DCH];
                     int row[G];
 #pragma unroll
@@ -781,7 +809,25 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
                 __syncwarp();
                 if (ctx_writes) {
                     for (int i = 0; i < nb; ++i) {
-                        const int xo = __shfl_sync(kFull, xid, i) * d4;
+                        const int x = __shfl_sync(kFull, xid, i);
+                        if (CTX && ((hot_ctx >> i) & 1u)) {  // merge into the CTA's cached delta
+                            touched_cache = true;
+                            if (lane == 0)
+                                while (atomicCAS(&locks0[x], 0, 1) != 0) {
+                                }
+                            __syncwarp();
+                            __threadfence_block();
+#pragma unroll
+                            for (int k = 0; k < DCH; ++k) {
+                                const int q = lane + 32 * k;
+                                if (in_row<DCH>(k, q, d4)) dblk0[x * d4 + q] = add4(dblk0[x * d4 + q], Hs[i * d4 + q]);
+                            }
+                            __threadfence_block();
+                            __syncwarp();
+                            if (lane == 0) atomicExch(&locks0[x], 0);
+                            continue;
+                        }
+                        const int xo = x * d4;
 #pragma unroll
                         for (int k = 0; k < DCH; ++k) {
                             const int q = lane + 32 * k;
@@ -817,14 +863,14 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
         last = atomicAdd(&s_done, 1) == workers - 1;
     }
     last = __shfl_sync(kFull, last, 0);
-    if (a.flusher && last && K > 0) {  // wake the flusher for its final flush
+    if (a.flusher && last && (K > 0 || K0 > 0)) {  // wake the flusher for its final flush
         __threadfence_block();
         named_bar_arrive(1, 64);
         return;
     }
     // without a flusher warp, the last worker to finish drains what the others merged
     // after their last flush
-    if (!a.flusher && last && K > 0) {
+    if (!a.flusher && last && (K > 0 || K0 > 0)) {
         __threadfence_block();
         flush_cache();
     }
@@ -841,22 +887,25 @@ constexpr int kW4 = DCH == 1 ? 16 : (DCH == 2 ? 12 : 8);
 
 // Row widths with a specialised K1 (D = 100, 128, 200, 300: the benchmark configurations,
 // rows padded to 32 bytes).
-template <int DCH>
-auto hog4_for(int d4) -> decltype(&hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>) {
-    if constexpr (DCH == 1) {
-        if (d4 == 26) return hog4_kernel<1, kG4<1>, kW4<1>, 26>;
-        if (d4 == 32) return hog4_kernel<1, kG4<1>, kW4<1>, 32>;
-    } else if constexpr (DCH == 2) {
-        if (d4 == 50) return hog4_kernel<2, kG4<2>, kW4<2>, 50>;
-    } else if constexpr (DCH == 3) {
-        if (d4 == 76) return hog4_kernel<3, kG4<3>, kW4<3>, 76>;
+template <int DCH, bool CTX>
+auto hog4_for(int d4, bool specialise) -> decltype(&hog4_kernel<DCH, kG4<DCH>, kW4<DCH>, 0, CTX>) {
+    if (specialise) {
+        if constexpr (DCH == 1) {
+            if (d4 == 26) return hog4_kernel<1, kG4<1>, kW4<1>, 26, CTX>;
+            if (d4 == 32) return hog4_kernel<1, kG4<1>, kW4<1>, 32, CTX>;
+        } else if constexpr (DCH == 2) {
+            if (d4 == 50) return hog4_kernel<2, kG4<2>, kW4<2>, 50, CTX>;
+        } else if constexpr (DCH == 3) {
+            if (d4 == 76) return hog4_kernel<3, kG4<3>, kW4<3>, 76, CTX>;
+        }
     }
-    return hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>;
+    return hog4_kernel<DCH, kG4<DCH>, kW4<DCH>, 0, CTX>;
 }
 
 template <int DCH, int G, int WORKERS>
 void launch_variant(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS> : (g.specialise ? hog4_for<DCH>(a.d4) : hog4_kernel<DCH, kG4<DCH>, kW4<DCH>>);
+    void (*k)(HogArgs) = g.kernel == 3 ? hog_kernel<DCH, G, WORKERS>
+                         : (g.ctx_rows > 0 ? hog4_for<DCH, true>(a.d4, g.specialise) : hog4_for<DCH, false>(a.d4, g.specialise));
     // always opt in: dynamic + static shared memory above 48 KB needs it even when the
     // dynamic part alone is below (a launch without it failed with "invalid argument")
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
@@ -905,8 +954,13 @@ void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches) {
 // Every hot row can be cached (row-major processing has no private-prefix depth limit).
 int hog_hmax(int) { return 1 << 30; }
 
+int hog_max_warps(int d4) {
+    const int v = (d4 + 31) / 32;
+    return v == 1 ? kW4<1> : (v == 2 ? kW4<2> : kW4<3>);
+}
+
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window, int kernel, int64_t tokens) {
+                     int rows_override, int window, int kernel, int64_t tokens, int ctx_rows) {
     HogGeometry g{};
     g.kernel = kernel == 3 ? 3 : 4;
     g.specialise = true;
@@ -926,7 +980,9 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     int rows = std::min(cache_rows_wanted, static_cast<int>((48 * 1024) / per_row));
     if (rows_override >= 0 && rows_override < rows) rows = rows_override;
     g.cache_rows = std::max(rows, 0);
-    const size_t cache_bytes = static_cast<size_t>(g.cache_rows) * d4 * 16 + static_cast<size_t>((g.cache_rows + 3) & ~3) * 4;
+    g.ctx_rows = g.kernel == 4 ? std::max(ctx_rows, 0) : 0;
+    const size_t cache_bytes = static_cast<size_t>(g.cache_rows) * d4 * 16 + static_cast<size_t>((g.cache_rows + 3) & ~3) * 4 +
+                               static_cast<size_t>(g.ctx_rows) * d4 * 16 + static_cast<size_t>((g.ctx_rows + 3) & ~3) * 4 + 128;
     // v4 also stages each warp's next row group (4 rows) in shared memory. A center whose
     // 2b contexts do not fit one context batch re-reads (and re-writes) its whole path per
     // batch: unless the caller fixed the warp count, drop one warp if that lets one batch
@@ -961,7 +1017,7 @@ HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int war
     // grows with the ticket: C1 3.33 ms at 8, 3.44 at 32).
     if (cpw_override <= 0) g.cpw = tokens / (static_cast<int64_t>(g.blocks) * g.warps) >= 2000 ? 16 : 8;
     // a warp the registers allow but shared memory cannot feed becomes the cache flusher
-    g.flusher = g.kernel == 4 && g.warps < workers && g.cache_rows > 0;
+    g.flusher = g.kernel == 4 && g.warps < workers && (g.cache_rows > 0 || g.ctx_rows > 0);
     return g;
 }
 

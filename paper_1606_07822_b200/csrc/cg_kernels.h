@@ -110,10 +110,11 @@ struct HogArgs {
     int32_t window;
     uint64_t win_key;
     int32_t cache_rows;        // K rows cached in shared memory (rows [0, K))
+    int32_t ctx_cache_rows;    // syn0 rows [0, K0) -- the most frequent words -- cached per CTA too
     int32_t centers_per_warp;
     int32_t cold_store;        // 1: plain stores for cold rows and syn0 (lossy Hogwild)
     float hot_flush_scale;     // multiplier on block-cache deltas at flush (if row_scale == nullptr)
-    const float* row_scale;    // per cached row flush multiplier, or nullptr
+    const float* row_scale;    // per cached row flush multiplier (syn1 rows, then syn0 rows), or nullptr
     int32_t flush_centers;     // centers merged into a block cache between flushes
     int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
     int32_t ctx_batch;         // context rows staged per warp (<= 2 * window)
@@ -131,13 +132,19 @@ struct HogGeometry {
     int kernel;     // 4 = hog4_kernel (default), 3 = hog_kernel
     bool specialise;  // v4: use the row-width-specialised instantiation when there is one
     bool flusher;     // v4: one extra (flusher) warp; only when registers leave room for it
+    int ctx_rows;     // v4: cached syn0 rows (most frequent context words)
     size_t smem;
 };
 // Depth limit on cached hot rows for this row width (none for the row-major kernel).
 int hog_hmax(int d4);
 // Picks the kernel variant for d4 and the launch geometry for the device.
+// Most frequent words whose syn0 rows K1 caches per CTA (averaged at flush, like the hot
+// syn1 rows): thousands of warps otherwise add stale updates to them at once.
+constexpr int kCtxCacheRows = 16;
+// Warps per CTA the registers allow for this row width (v4).
+int hog_max_warps(int d4);
 HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window, int kernel, int64_t tokens);
+                     int rows_override, int window, int kernel, int64_t tokens, int ctx_rows);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 // ---------------- evaluation (cg_eval.cu) -----------------------------------------

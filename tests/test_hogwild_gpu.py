@@ -145,3 +145,21 @@ def test_hogwild_every_kernel_variant_learns(dim, window, probe):
     init = api.init_model(vocab.size(), dim, 11)
     li, ld, lh = (_loss(x, tree, vocab, ids, c) for x in (init, det, m))
     assert li - lh > 0.9 * (li - ld), (lh, ld, li, e.worker_warps, e.ctx_batch, e.cached_rows)
+
+
+def test_hogwild_without_subsampling_matches_reference_c1():
+    """sample = 0 (no subsampling): the most frequent words then sit in the windows of
+    thousands of concurrently training warps. Their syn0 rows and the hot syn1 rows are
+    cached per CTA and averaged at flush; summing the stale updates diverged. The loss must
+    match the reference's single-stream training within the north-star 2%."""
+    c, vocab, ids = c1()
+    tree, sel = setup(vocab)
+    cfg = dict(dim=c.dim, window=c.window, min_count=1, sample=0.0, iterations=1, cache_nodes=31,
+               flush_interval=10, seed=1)
+    ref0, ref1, _ = O.orc_train(ids, vocab.counts, vocab.total_tokens(), cfg)
+    cz = CorpusConfig("c1-nosample", c.tokens, c.vocab, c.zipf_s, c.dim, c.window, 0.0, 1, c.seed)
+    ref_loss = _loss(api.Model(vocab.size(), c.dim, ref0, ref1), tree, vocab, ids, cz)
+    m = api.train(ids, vocab, tree, sel, api.TrainConfig(**cfg, mode="hogwild"))
+    assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
+    gpu_loss = _loss(m, tree, vocab, ids, cz)
+    assert abs(gpu_loss - ref_loss) / ref_loss < 0.02, (gpu_loss, ref_loss)

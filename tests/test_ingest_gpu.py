@@ -177,10 +177,12 @@ def test_hogwild_train_from_file_ramped_chunks(tmp_path):
     read, covering every token once, with the same id stream as the host reader."""
     rng = np.random.default_rng(21)
     words = np.array([f"w{i}" for i in range(20000)])
+    p = 1.0 / np.arange(1, 20001)
+    p /= p.sum()  # Zipf(1.0) truncated to 20k types
     path = str(tmp_path / "r.txt")
     with open(path, "w") as f:
-        for _ in range(7):
-            f.write(" ".join(words[np.minimum(rng.zipf(1.1, 400_000), 20000) - 1]) + "\n")
+        for _ in range(8):
+            f.write(" ".join(words[rng.choice(20000, 400_000, p=p)]) + "\n")
     assert Path(path).stat().st_size > 12 << 20
     vocab = api.build_vocabulary_file(path, 1)
     ids = api.read_id_stream(path, vocab)
