@@ -1,3 +1,6 @@
+"""Stability of K1 without subsampling: C1/C2 with sample 0 and with their own sample,
+with the hot syn0-row cache (default) and without it (probe bit 6); prints finiteness and
+HS loss against the untrained model's.  python tools/stability_probe.py"""
 import sys, numpy as np
 sys.path.insert(0, "."); sys.path.insert(0, "tests")
 import oracle_lib as O, bench
