@@ -30,10 +30,6 @@
 #include "cachegram/model.hpp"
 #include "cachegram/trainer.hpp"
 #include "cachegram_b200.h"
-
-#ifndef CG_FLUSH_T
-#define CG_FLUSH_T 1.0  // CTA replicas of a cached row whose deltas are summed, not averaged, at flush
-#endif
 #include "cg_device.cuh"
 #include "cg_host.h"
 #include "cg_kernels.h"
@@ -868,7 +864,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                     std::vector<float> sc(static_cast<size_t>(g.cache_rows + g.ctx_rows));
                     auto scale_of = [&](double q) {
                         const double p = 1.0 - std::pow(1.0 - std::min(q, 1.0), static_cast<double>(h.flush_centers));
-                        return static_cast<float>(1.0 / std::max(1.0, p * g.blocks / CG_FLUSH_T));
+                        return static_cast<float>(1.0 / std::max(1.0, p * g.blocks));
                     };
                     for (int32_t r = 0; r < g.cache_rows; ++r)
                         sc[static_cast<size_t>(r)] =
