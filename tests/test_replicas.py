@@ -137,3 +137,30 @@ def test_bench_two_ranks_functional(tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "replicas2"
     assert d["e2e"]["value"] > 0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_nccl_on_two_gpus():
+    """The driver's N > 1 launch exactly (NCCL, one rank per GPU); runs only where at
+    least two GPUs are visible (the round-1 boxes have one)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    root = Path(__file__).resolve().parents[1]
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(root / "bench.py"), "--gpus", "2",
+           "--config", "c1", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--e2e-steps", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(root),
+                       env=dict(os.environ, MASTER_ADDR="127.0.0.1"))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak" and d["e2e"]["value"] > 0
