@@ -135,6 +135,13 @@ struct DevBuf {
 };
 
 // ---- small device helpers of the layout --------------------------------------
+__global__ void path_code_kernel(const int32_t* nodes, const uint8_t* turns, const int32_t* row_of_node, int64_t n,
+                                 int32_t* code) {
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        code[k] = (row_of_node[nodes[k]] << 1) | turns[k];
+}
+
 __global__ void init_syn0_kernel(float* out, int64_t rows, int32_t dim, int32_t stride, uint64_t key, float inv_dim) {
     // model.hpp:66-72: value i (row-major, unpadded) = (unit24(draw i) - 0.5f) * (1/D)
     const int64_t n = rows * dim;
@@ -484,6 +491,12 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
     *out = nullptr;
     auto s = std::make_unique<cg_session>();
     const int rc = guarded([&] {
+        const auto tp0 = std::chrono::steady_clock::now();
+        auto tmark = [&](const char* what) {
+            if (std::getenv("CG_PROFILE"))
+                std::fprintf(stderr, "  create: %-12s %.2f ms\n", what,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
+        };
         if (!cfg || !md) invalid("null config or model");
         validate_config(*cfg);
         validate_model(*md);
@@ -512,11 +525,13 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
         for (int32_t w = 0; w < V; ++w)
             s->max_depth = std::max<int32_t>(s->max_depth, static_cast<int32_t>(md->path_offsets[w + 1] - md->path_offsets[w]));
         for (auto& e : s->ev) CG_CUDA(cudaEventCreate(&e));
+        tmark("validated");
 
         const cachegram::SigmoidTable table;
         s->sigmoid.upload(table.data(), 1000, s->stream);
+        std::vector<float> kp;
         if (cfg->sample > 0.0) {
-            std::vector<float> kp(static_cast<size_t>(V));
+            kp.resize(static_cast<size_t>(V));
             for (int32_t w = 0; w < V; ++w)
                 kp[static_cast<size_t>(w)] =
                     static_cast<float>(cachegram::keep_probability(md->counts[w], md->total_tokens, cfg->sample));
@@ -527,7 +542,7 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             double kept_total = 0.0;
             std::vector<double> kept(static_cast<size_t>(std::min<int32_t>(V, cgk::kCtxCacheRows)));
             for (int32_t w = 0; w < V; ++w) {
-                const double kpw = cfg->sample > 0.0 ? std::min(1.0, cachegram::keep_probability(md->counts[w], md->total_tokens, cfg->sample)) : 1.0;
+                const double kpw = kp.empty() ? 1.0 : std::min(1.0, static_cast<double>(kp[static_cast<size_t>(w)]));
                 const double k = static_cast<double>(md->counts[w]) * kpw;
                 kept_total += k;
                 if (w < static_cast<int32_t>(kept.size())) kept[static_cast<size_t>(w)] = k;
@@ -561,10 +576,12 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             // by (usage desc, id asc); one extra all-zero row pads cold-step groups.
             const int hmax = cgk::hog_hmax(s->Dp / 4);
             std::vector<int32_t> depth(static_cast<size_t>(V - 1), 0);
-            for (int32_t w = 0; w < V; ++w)
-                for (int64_t k = md->path_offsets[w]; k < md->path_offsets[w + 1]; ++k)
-                    depth[static_cast<size_t>(md->path_nodes[k])] = static_cast<int32_t>(k - md->path_offsets[w]);
+            if (hmax <= s->max_depth)  // only a depth limit below the deepest path needs depths
+                for (int32_t w = 0; w < V; ++w)
+                    for (int64_t k = md->path_offsets[w]; k < md->path_offsets[w + 1]; ++k)
+                        depth[static_cast<size_t>(md->path_nodes[k])] = static_cast<int32_t>(k - md->path_offsets[w]);
             std::vector<char> placed(static_cast<size_t>(V - 1), 0);
+            tmark("keep+depth");
             s->node_of_row.reserve(static_cast<size_t>(V - 1));
             for (int32_t k = 0; k < s->K; ++k) {
                 const int32_t n = md->hot_nodes[k];
@@ -580,9 +597,9 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             std::vector<int32_t> rest;
             for (int32_t n = 0; n < V - 1; ++n)
                 if (!placed[static_cast<size_t>(n)]) rest.push_back(n);
-            if (md->node_usage)
-                std::stable_sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
-                    return md->node_usage[a] > md->node_usage[b];
+            if (md->node_usage)  // usage descending, id ascending on ties (rest is in id order)
+                std::sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
+                    return md->node_usage[a] != md->node_usage[b] ? md->node_usage[a] > md->node_usage[b] : a < b;
                 });
             s->node_of_row.insert(s->node_of_row.end(), rest.begin(), rest.end());
             constexpr int32_t kMinCachedRows = 31;
@@ -594,20 +611,33 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             }
             s->row_of_node.assign(static_cast<size_t>(V - 1), 0);
             for (int32_t r = 0; r < V - 1; ++r) s->row_of_node[static_cast<size_t>(s->node_of_row[static_cast<size_t>(r)])] = r;
-            std::vector<int32_t> off(static_cast<size_t>(V) + 1), code(static_cast<size_t>(steps));
+            std::vector<int32_t> off(static_cast<size_t>(V) + 1);
             for (int32_t w = 0; w <= V; ++w) off[static_cast<size_t>(w)] = static_cast<int32_t>(md->path_offsets[w]);
-            for (int64_t k = 0; k < steps; ++k)
-                code[static_cast<size_t>(k)] = (s->row_of_node[static_cast<size_t>(md->path_nodes[k])] << 1) | md->path_turns[k];
             s->hw_off.upload(off.data(), off.size(), s->stream);
-            s->hw_code.upload(code.data(), code.size(), s->stream);
             s->node_of_row_dev.upload(s->node_of_row.data(), s->node_of_row.size(), s->stream);
             s->row_of_node_dev.upload(s->row_of_node.data(), s->row_of_node.size(), s->stream);
+            // path codes (device row << 1 | turn), translated on the device from the tree's
+            // node ids and turns (a host pass over every path step took ~1 ms at C2)
+            {
+                DevBuf<int32_t> nodes;
+                DevBuf<uint8_t> turns;
+                nodes.upload(md->path_nodes, static_cast<size_t>(steps), s->stream);
+                turns.upload(md->path_turns, static_cast<size_t>(steps), s->stream);
+                s->hw_code.alloc(static_cast<size_t>(steps));
+                path_code_kernel<<<grid_for(steps), 256, 0, s->stream>>>(nodes.p, turns.p, s->row_of_node_dev.p, steps,
+                                                                          s->hw_code.p);
+                CG_CUDA(cudaGetLastError());
+                CG_CUDA(cudaStreamSynchronize(s->stream));  // before the staging buffers go
+            }
+            tmark("row order");
             // syn0 [V rows] then syn1 [V-1 rows + 1 zero pad row]
             s->model.alloc(static_cast<size_t>(V) * s->Dp + static_cast<size_t>(V) * s->Dp);
             s->counters.alloc(4);
         }
+        tmark("alloc");
         session_reset_model(*s);
         CG_CUDA(cudaStreamSynchronize(s->stream));
+        tmark("reset+sync");
     });
     if (rc == CG_OK) *out = s.release();
     return rc;
