@@ -64,7 +64,7 @@ def main():
         if "lts__t_sectors.sum" in h:
             l2 = float(row[h.index("lts__t_sectors.sum")].replace(",", "")) * 32.0
             t_ms = float(row[h.index("gpu__time_duration.sum")].replace(",", ""))
-            t_s = t_ms * {"ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6, "ns": 1e-9, "nsecond": 1e-9}.get(
+            t_s = t_ms * {"s": 1.0, "second": 1.0, "ms": 1e-3, "msecond": 1e-3, "us": 1e-6, "usecond": 1e-6, "ns": 1e-9, "nsecond": 1e-9}.get(
                 units[h.index("gpu__time_duration.sum")], 1e-3)
             print(f"L2 traffic per launch: {l2:.4g} bytes (lts__t_sectors x 32 B) = {l2 / t_s / 1e9:.0f} GB/s")
         print()
