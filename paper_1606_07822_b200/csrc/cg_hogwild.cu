@@ -32,6 +32,10 @@
 #include "cg_kernels.h"
 
 
+#ifndef CG_W2
+#define CG_W2 12  // warps per CTA the D <= 256 variant is compiled for (experiments: tools/ab_build.py)
+#endif
+
 namespace cgk {
 namespace {
 
@@ -883,7 +887,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog4_kernel(HogArgs a) {
 template <int DCH>
 constexpr int kG4 = 4;
 template <int DCH>
-constexpr int kW4 = DCH == 1 ? 16 : (DCH == 2 ? 12 : 8);
+constexpr int kW4 = DCH == 1 ? 16 : (DCH == 2 ? CG_W2 : 8);
 
 // Row widths with a specialised K1 (D = 100, 128, 200, 300: the benchmark configurations,
 // rows padded to 32 bytes).
