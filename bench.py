@@ -53,10 +53,9 @@ def parse():
     p.add_argument("--cpw", type=int, default=0)
     p.add_argument("--rows", type=int, default=-1)
     p.add_argument("--blocks", type=int, default=0)
-    p.add_argument("--cold-update", type=int, default=0)
     p.add_argument("--hot-flush-scale", type=float, default=0.0)
-    p.add_argument("--kernel", type=int, default=0, help="K1 version: 0 default, 3 = v3 per-context kernel")
-    p.add_argument("--probe", type=int, default=0, help="K1 experiment bits (cg_tuning.probe); 0 for real runs")
+    p.add_argument("--flush-centers", type=int, default=0)
+    p.add_argument("--min-cache-rows", type=int, default=0)
     return p.parse_args()
 
 
@@ -282,8 +281,8 @@ def main():
                           cache_nodes=args.cache_nodes, seed=c.seed, mode="hogwild")
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
-    sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.cold_update, args.hot_flush_scale, kernel=args.kernel,
-              probe=args.probe)
+    sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.hot_flush_scale, args.flush_centers,
+              args.min_cache_rows)
     if isinstance(ids, np.ndarray):
         sess.upload_ids(ids)
     else:
@@ -307,7 +306,8 @@ def main():
             agg["kept"] += e.kept
             agg["launch_count"] += e.train_launches
             agg["geometry"] = {"blocks": e.blocks, "worker_warps": e.worker_warps, "ctx_batch": e.ctx_batch,
-                               "cached_rows_per_cta": e.cached_rows}
+                               "cached_rows_per_cta": e.cached_rows, "smem_rows": e.smem_rows,
+                               "floor_rows": e.floor_rows, "flush_centers": e.flush_centers}
         return e
 
     from paper_1606_07822_b200.replicas import ReplicaTrainer

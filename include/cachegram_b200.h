@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define CG_ABI_VERSION 2  /* 2: cg_epoch_stats reports the K1 launch geometry */
+#define CG_ABI_VERSION 3  /* 3: two-tier per-CTA cache honouring K and u; cg_tuning without experiment bits */
 
 /* The library is built with -fvisibility=hidden; only these entry points are exported. */
 #if defined(__GNUC__)
@@ -63,8 +63,15 @@ typedef struct cg_config {
     float alpha0;
     int32_t iterations;
     int32_t workers;        /* reference CPU thread count; the GPU path ignores it */
-    int32_t cache_nodes;    /* K */
-    int32_t flush_interval; /* u, in trained centers (deterministic mode) */
+    int32_t cache_nodes;    /* K: the paper's node cache (trainer.hpp:33). HOGWILD: every CTA caches the K
+                               CacheSelection rows -- the hottest (default 8) in shared memory, the
+                               rest as CTA-private delta rows in L2 -- plus the stability floor
+                               (cg_tuning.min_cache_rows). Flushes add each row's delta scaled by
+                               1 / E[#CTAs contributing per flush period]: rows few CTAs touch are
+                               summed as in the reference, the CTA replicas of hot rows are
+                               averaged. cg_epoch_stats reports the rows cached. */
+    int32_t flush_interval; /* u, in trained centers per worker (trainer.hpp:34, 127). HOGWILD: a CTA's
+                               cache is drained every u x (its worker warps) merged centers. */
     uint64_t seed;
 } cg_config;
 
@@ -177,10 +184,14 @@ typedef struct cg_epoch_stats {
     double subsample_ms;     /* device time of subsampling + compaction */
     int32_t train_launches;  /* kernels launched by this call */
     int32_t other_launches;
-    int32_t cached_rows;     /* hogwild: syn1 rows held in each CTA's shared-memory cache */
+    int32_t cached_rows;     /* hogwild: syn1 rows cached per CTA (both tiers) = max(K, floor_rows) */
     int32_t worker_warps;    /* hogwild: worker warps per CTA */
     int32_t ctx_batch;       /* hogwild: contexts staged per batch */
     int32_t blocks;          /* hogwild: persistent CTAs */
+    int32_t smem_rows;       /* hogwild: of cached_rows, those held in shared memory (the rest: L2 tier) */
+    int32_t floor_rows;      /* hogwild: the stability floor of this launch (0 when disabled) */
+    int32_t flush_centers;   /* hogwild: merged centers per CTA between flushes (u x worker warps) */
+    int32_t pad;
 } cg_epoch_stats;
 
 /* stream: a cudaStream_t (NULL = legacy default stream). device: CUDA ordinal. */
@@ -207,27 +218,21 @@ CG_API int cg_session_train(cg_session* s, cg_train_stats* stats);
 CG_API int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out);
 /* The device model buffer (for an all-reduce between replicas) and its geometry. */
 CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int32_t* row_stride_floats);
-/* Hogwild kernel knobs (zero-initialised = defaults). For tuning and experiments. */
+/* Hogwild kernel knobs (zero-initialised = defaults, except smem_cache_rows: -1). */
 typedef struct cg_tuning {
     int32_t blocks;           /* 0 = one persistent CTA per SM */
     int32_t warps_per_block;  /* 0 = the variant's maximum */
     int32_t centers_per_warp; /* 0 = auto: consecutive kept centers per work ticket (16, or 8 for small passes) */
-    int32_t smem_cache_rows;  /* < 0 = min(K, what fits); hot rows held in the block cache */
-    int32_t cold_update;      /* 0 = red.global.add (no lost updates), 1 = plain store (lossy, as the reference) */
+    int32_t smem_cache_rows;  /* < 0 = 8: how many of the cached rows live in shared memory (capped at 48 KB of
+                                 rows); the others are CTA-private delta rows in L2 */
     float hot_flush_scale;    /* 0 = per-row 1/E[#CTAs contributing per flush] (averaging of overlapping
                                  CTA replicas); > 0 = this multiplier for every cached row */
-    int32_t flush_centers;    /* 0 = 128: centers merged into a CTA's cache between flushes */
-    int32_t min_cache_rows;   /* 0 = default: each CTA caches the top 8 rows (K picks them, the top 31 rows
-                                 by usage follow); > 0 = cache max(8, this) rows, at most max(K, 31);
-                                 < 0 = honour K exactly,
-                                 even K = 0 (unstable at full-GPU concurrency; experiments only) */
-    int32_t probe;            /* experiments only (breaks training): bit 0 skip cold-row updates, bit 1 skip
-                                 context-row updates, bit 2 skip cache merges, bit 3 skip reading the
-                                 CTA's cached deltas; bit 4 (harmless) flushes the cache from the workers
-                                 even when a flusher warp fits; bit 5 (harmless) runs the generic-width K1
-                                 instead of the one specialised for D = 100/128/200/300; bit 6 does not
-                                 cache the most frequent words' syn0 rows (unstable without subsampling) */
-    int32_t kernel;           /* 0 = default (4: center-batched row groups), 3 = the v3 per-context kernel */
+    int32_t flush_centers;    /* 0 = u x worker warps: merged centers per CTA between flushes */
+    int32_t min_cache_rows;   /* the stability floor: 0 = auto, the leading rows whose expected concurrent
+                                 updaters (share of paths x warps in flight) reach 256 are cached even when
+                                 K is smaller; > 0 = at least this many rows; < 0 = none, K is honoured
+                                 literally (K = 0 then diverges on small vocabularies at full-GPU
+                                 concurrency) */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 

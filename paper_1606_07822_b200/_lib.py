@@ -89,14 +89,17 @@ class CgEpochStats(C.Structure):
         ("worker_warps", C.c_int32),
         ("ctx_batch", C.c_int32),
         ("blocks", C.c_int32),
+        ("smem_rows", C.c_int32),
+        ("floor_rows", C.c_int32),
+        ("flush_centers", C.c_int32),
+        ("pad", C.c_int32),
     ]
 
 
 class CgTuning(C.Structure):
     _fields_ = [("blocks", C.c_int32), ("warps_per_block", C.c_int32), ("centers_per_warp", C.c_int32),
-                ("smem_cache_rows", C.c_int32), ("cold_update", C.c_int32), ("hot_flush_scale", C.c_float),
-                ("flush_centers", C.c_int32), ("min_cache_rows", C.c_int32), ("probe", C.c_int32),
-                ("kernel", C.c_int32)]
+                ("smem_cache_rows", C.c_int32), ("hot_flush_scale", C.c_float), ("flush_centers", C.c_int32),
+                ("min_cache_rows", C.c_int32)]
 
 
 P = C.POINTER

@@ -108,9 +108,15 @@ void validate_model(const cg_model_desc& m) {
     for (int64_t k = 0; k < steps; ++k)
         if (m.path_nodes[k] < 0 || m.path_nodes[k] >= m.vocab_size - 1 || m.path_turns[k] > 1)
             invalid("vocabulary and tree sizes disagree");
-    for (int32_t s = 0; s < m.hot_count; ++s)
-        if (m.hot_nodes[s] < 0 || m.hot_nodes[s] >= m.vocab_size - 1)
+    std::vector<char> seen(static_cast<size_t>(m.vocab_size - 1), 0);
+    for (int32_t s = 0; s < m.hot_count; ++s) {
+        if (m.hot_nodes[s] < 0 || m.hot_nodes[s] >= m.vocab_size - 1 || seen[static_cast<size_t>(m.hot_nodes[s])])
             invalid("cache selection was built from a different tree");
+        seen[static_cast<size_t>(m.hot_nodes[s])] = 1;
+    }
+    // HuffmanTree::node_usage orders the device rows and sets the flush scale of every
+    // cached row; without it the hot rows' CTA replicas would be summed (divergent).
+    if (!m.node_usage) invalid("model description has null arrays");
 }
 
 
@@ -213,12 +219,16 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    cg_tuning tune{0, 0, 0, -1, 0, 0.0f, 0, 0, 0};
-    int32_t cached_rows = 0;  // hogwild: rows [0, cached_rows) of syn1 are eligible for the CTA cache
-    std::vector<double> row_share;  // hogwild: usage share (of the root's) of the cache-eligible rows
+    cg_tuning tune{0, 0, 0, -1, 0.0f, 0, 0};
+    // hogwild: share of the paths through device row r (usage / root usage), for the first
+    // min(V-1, kMaxCacheRows) rows (the cacheable ones; device rows are in usage order
+    // after the caller's selection)
+    std::vector<double> row_share;
+    DevBuf<float> tier2;  // hogwild: the L2 tier of the per-CTA cache (zeroed before each launch)
     std::vector<double> ctx_share;  // hogwild: share of centers with word w (w < kCtxCacheRows) in their window
     DevBuf<float> row_scale;
-    int scale_blocks = -1, scale_flush = -1, scale_rows = -1;
+    int scale_blocks = -1, scale_flush = -1;
+    int64_t scale_rows = -1;
 
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
@@ -567,48 +577,30 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             }
             s->det_state.alloc(1);
         } else {
-            if (s->Dp > 4 * 96) invalid("hogwild mode supports dim <= 384");
-            if (s->max_depth > 64) invalid("hogwild mode supports Huffman depth <= 64");
             if (steps >= (int64_t{1} << 31)) invalid("tree too large for 32-bit path offsets");
-            // Device row order: first the hot rows (CacheSelection slot order) whose depth is
-            // below the kernel's private-prefix depth HMAX -- the rows the per-CTA cache
-            // holds, so "cached" is simply row < cached_rows -- then every other inner node
-            // by (usage desc, id asc); one extra all-zero row pads cold-step groups.
-            const int hmax = cgk::hog_hmax(s->Dp / 4);
-            std::vector<int32_t> depth(static_cast<size_t>(V - 1), 0);
-            if (hmax <= s->max_depth)  // only a depth limit below the deepest path needs depths
-                for (int32_t w = 0; w < V; ++w)
-                    for (int64_t k = md->path_offsets[w]; k < md->path_offsets[w + 1]; ++k)
-                        depth[static_cast<size_t>(md->path_nodes[k])] = static_cast<int32_t>(k - md->path_offsets[w]);
+            if (V >= (1 << 30)) invalid("vocabulary too large for 30-bit device row ids");
+            // Device row order: the CacheSelection's rows in slot order (the per-CTA cache
+            // holds device rows [0, K), so "cached" is simply row < K), then every other
+            // inner node by (usage desc, id asc); one extra all-zero row pads row groups.
             std::vector<char> placed(static_cast<size_t>(V - 1), 0);
-            tmark("keep+depth");
             s->node_of_row.reserve(static_cast<size_t>(V - 1));
             for (int32_t k = 0; k < s->K; ++k) {
-                const int32_t n = md->hot_nodes[k];
-                if (depth[static_cast<size_t>(n)] < hmax) {
-                    s->node_of_row.push_back(n);
-                    placed[static_cast<size_t>(n)] = 1;
-                }
+                s->node_of_row.push_back(md->hot_nodes[k]);
+                placed[static_cast<size_t>(md->hot_nodes[k])] = 1;
             }
-            // The GPU always caches at least the top kMinCachedRows rows: uncached, the
-            // top-of-tree rows see ~10^3 concurrent stale updates and training diverges
-            // (DESIGN.md 3). Rows beyond the caller's selection follow in usage order.
-            s->cached_rows = static_cast<int32_t>(s->node_of_row.size());
             std::vector<int32_t> rest;
+            rest.reserve(static_cast<size_t>(V - 1 - s->K));
             for (int32_t n = 0; n < V - 1; ++n)
                 if (!placed[static_cast<size_t>(n)]) rest.push_back(n);
-            if (md->node_usage)  // usage descending, id ascending on ties (rest is in id order)
-                std::sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
-                    return md->node_usage[a] != md->node_usage[b] ? md->node_usage[a] > md->node_usage[b] : a < b;
-                });
+            std::sort(rest.begin(), rest.end(), [md](int32_t a, int32_t b) {
+                return md->node_usage[a] != md->node_usage[b] ? md->node_usage[a] > md->node_usage[b] : a < b;
+            });
             s->node_of_row.insert(s->node_of_row.end(), rest.begin(), rest.end());
-            constexpr int32_t kMinCachedRows = 31;
-            s->cached_rows = std::max(s->cached_rows, std::min(kMinCachedRows, V - 1));
-            if (md->node_usage) {
-                const double root = static_cast<double>(md->node_usage[V - 2]);
-                for (int32_t r = 0; r < s->cached_rows; ++r)
-                    s->row_share.push_back(static_cast<double>(md->node_usage[s->node_of_row[static_cast<size_t>(r)]]) / root);
-            }
+            tmark("row order");
+            const double root = std::max(1.0, static_cast<double>(md->node_usage[V - 2]));
+            const int32_t nshare = std::min<int32_t>(V - 1, cgk::kMaxCacheRows);
+            for (int32_t r = 0; r < nshare; ++r)
+                s->row_share.push_back(static_cast<double>(md->node_usage[s->node_of_row[static_cast<size_t>(r)]]) / root);
             s->row_of_node.assign(static_cast<size_t>(V - 1), 0);
             for (int32_t r = 0; r < V - 1; ++r) s->row_of_node[static_cast<size_t>(s->node_of_row[static_cast<size_t>(r)])] = r;
             std::vector<int32_t> off(static_cast<size_t>(V) + 1);
@@ -629,7 +621,7 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                 CG_CUDA(cudaGetLastError());
                 CG_CUDA(cudaStreamSynchronize(s->stream));  // before the staging buffers go
             }
-            tmark("row order");
+            tmark("path codes");
             // syn0 [V rows] then syn1 [V-1 rows + 1 zero pad row]
             s->model.alloc(static_cast<size_t>(V) * s->Dp + static_cast<size_t>(V) * s->Dp);
             s->counters.alloc(4);
@@ -768,7 +760,7 @@ int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int
 int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
         if (!t) invalid("null tuning");
-        if (t->cold_update < 0 || t->cold_update > 1) invalid("cold_update must be 0 or 1");
+        if (t->smem_cache_rows > cgk::kMaxCacheRows) invalid("smem_cache_rows out of range");
         s->tune = *t;
     });
 }
@@ -843,58 +835,82 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             h.window = s->cfg.window;
             h.win_key = cgdev::mix64(s->cfg.seed ^ 0x77696e646f77ull) + 0x9e3779b97f4a7c15ull * static_cast<uint64_t>(epoch + 1);
             h.counters = s->counters.p;
-            h.cold_store = s->tune.cold_update;
-            // Rows each CTA caches in shared memory. By default the top kGpuCacheRows rows,
-            // whatever K is: more cached rows cost more lock/merge/flush work than the
-            // red.global of a moderately hot row, and at D 300 they cost a worker warp
-            // (K1 sweep, profiles/r1_rows_sweep.jsonl: 8 rows is within 3% of the fastest at
-            // C1-C5, 31 rows is 3-16% slower; loss unchanged). K selects the rows (the
-            // CacheSelection order); min_cache_rows < 0 honours K exactly (the K sweep).
-            constexpr int32_t kGpuCacheRows = 8;
-            const int32_t want_rows =
-                s->tune.min_cache_rows < 0 ? s->K : std::min(s->cached_rows, std::max(kGpuCacheRows, s->tune.min_cache_rows));
+            // ---- the per-CTA cache (NodeCache, trainer.hpp:75-138) at GPU concurrency ----
+            // K = cache_nodes rows are cached: the CacheSelection's rows, which lead the
+            // device row order. K1 runs ~1500 warps at once, and a row on the paths of a
+            // share q of the centers then has ~q x 1500 concurrent updaters; uncached, the
+            // top-of-tree rows (q ~ 1) take ~10^3 stale updates at once and training
+            // diverges. So on top of K the cache always holds the leading rows
+            // whose expected concurrent updaters reach kHotUpdaters (the stability floor,
+            // cg_tuning.min_cache_rows; < 0 disables it, which honours K = 0 literally).
+            constexpr double kHotUpdaters = 256.0;
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+            const int blocks = s->tune.blocks > 0 ? s->tune.blocks : sms;
+            const double inflight = static_cast<double>(blocks) * cgk::hog_max_warps(s->Dp / 4, s->max_depth);
+            int32_t floor_rows = 0;
+            if (s->tune.min_cache_rows == 0) {
+                for (int32_t r = 0; r < static_cast<int32_t>(s->row_share.size()); ++r)
+                    if (s->row_share[static_cast<size_t>(r)] * inflight >= kHotUpdaters) floor_rows = r + 1;
+            } else if (s->tune.min_cache_rows > 0) {
+                floor_rows = s->tune.min_cache_rows;
+            }
+            const int32_t want_rows = std::min<int32_t>({std::max(s->K, floor_rows), s->V - 1, cgk::kMaxCacheRows});
             // The most frequent words' syn0 rows are cached too when their expected number of
             // concurrent updaters -- the share of centers with the word in their window x the
             // warps training at once -- reaches kHotUpdaters. Without subsampling (sample 0)
             // the top words of C1/C2 reach ~1400 and summed stale updates diverged; cached
             // and averaged, the loss matches the reference's (6.6130 vs 6.6128 at C1). With
             // subsampling no word of C1-C5 gets there, and averaging would slow their learning.
-            constexpr double kHotUpdaters = 256.0;
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
-            const double inflight = static_cast<double>(s->tune.blocks > 0 ? s->tune.blocks : sms) *
-                                    cgk::hog_max_warps(s->Dp / 4);
             int32_t ctx_rows = 0;
             while (ctx_rows < static_cast<int32_t>(s->ctx_share.size()) &&
                    s->ctx_share[static_cast<size_t>(ctx_rows)] * inflight >= kHotUpdaters)
                 ++ctx_rows;
-            if (s->tune.probe & 64) ctx_rows = 0;
-            h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers : 128;  // 32: +22% K1 time at C2, 64: +8%, 256: same as 128 (profiles/r1_perf4_c2.jsonl)
             h.dummy_row = s->V - 1;
-            h.probe = s->tune.probe;
-            cgk::HogGeometry g = cgk::hog_plan(h.d4, want_rows, s->tune.blocks, s->tune.warps_per_block,
-                                               s->tune.centers_per_warp, s->tune.smem_cache_rows, s->cfg.window,
-                                               s->tune.kernel, n, ctx_rows);
-            if (s->tune.probe & 32) g.specialise = false;  // experiments: the generic row width
-            if (s->tune.probe & 16) g.flusher = false;     // experiments: workers flush inline
-            // Each CTA trains its own replica of the hot rows between flushes; flushing
-            // delta / n_CTA averages the replicas (local SGD + model averaging, as across
-            // GPUs). Summing them (scale 1) is unstable at ~10^3 concurrent warps: every
-            // CTA pushes the same top-of-tree correction, overshooting by ~n_CTA.
+            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->max_depth, want_rows, s->tune.smem_cache_rows, s->tune.blocks,
+                                                     s->tune.warps_per_block, s->tune.centers_per_warp, s->cfg.window, n,
+                                                     ctx_rows);
+            if (g.smem == 0) invalid("dim too large for the generic kernel's shared-memory row buffers");
+            // flush_interval u (trainer.hpp:127): each worker warp flushes every u of its
+            // centers in the reference; here a CTA's workers share one cache, so it is
+            // drained every u x (worker warps) merged centers.
+            h.flush_centers = s->tune.flush_centers > 0 ? s->tune.flush_centers
+                                                          : std::max(1, s->cfg.flush_interval * g.warps);
+            // The L2 tier: rows [S, K) of every CTA's cache, zeroed before each launch (the
+            // kernel leaves it zero; re-zeroing keeps an aborted launch from leaking deltas).
+            const size_t t2n = static_cast<size_t>(g.blocks) *
+                               static_cast<size_t>(g.cache_rows - g.smem_rows) * s->Dp;
+            h.tier2 = nullptr;
+            if (t2n > 0) {
+                if (s->tier2.n < t2n) s->tier2.alloc(t2n);
+                CG_CUDA(cudaMemsetAsync(s->tier2.p, 0, t2n * sizeof(float), s->stream));
+                h.tier2 = s->tier2.p;
+            }
+            // Each CTA trains its own replica of the cached rows between flushes. The paper
+            // sums the workers' deltas (trainer.hpp:116-119); at GPU concurrency that sum is a
+            // step computed from one stale snapshot by every contributing CTA. A row on the
+            // paths of a share q of the centers gets, per flush period of F merged centers per
+            // CTA, about n_CTA x q x F such updates: for the root (q = 1) ~10^4, and summed they
+            // overshoot and diverge. The flush therefore scales each row's delta
+            // by s = min(1, max(1 / (p n_CTA), H / (n_CTA q F))): at most H = 32 stale updates'
+            // worth per flush (8x below where C1 diverged, profiles/r2_rule3_c1.jsonl), never
+            // less than the average of the p n_CTA contributing replicas (p = 1 - (1 - q)^F,
+            // the chance that a CTA touches the row in a period), and the plain sum of the
+            // reference for rows few CTAs touch.
             h.hot_flush_scale = s->tune.hot_flush_scale > 0.0f ? s->tune.hot_flush_scale : 1.0f / static_cast<float>(g.blocks);
-            // Default per-row scale: 1 / E[#CTAs contributing to the row per flush period].
-            // A row on the paths of a share q of the centers is touched by a CTA within F
-            // merged centers with probability 1 - (1 - q)^F; averaging over that many
-            // replicas keeps the hot rows stable while deep cached rows still sum.
             h.row_scale = nullptr;
-            h.ctx_cache_rows = g.ctx_rows;
             if (s->tune.hot_flush_scale <= 0.0f && (g.cache_rows > 0 || g.ctx_rows > 0)) {
-                if (s->scale_blocks != g.blocks || s->scale_flush != h.flush_centers || s->scale_rows != g.cache_rows * 4096 + g.ctx_rows) {
+                if (s->scale_blocks != g.blocks || s->scale_flush != h.flush_centers ||
+                    s->scale_rows != static_cast<int64_t>(g.cache_rows) * 4096 + g.ctx_rows) {
                     // syn1 cached rows [0, cache_rows), then the cached syn0 rows [0, ctx_rows)
                     std::vector<float> sc(static_cast<size_t>(g.cache_rows + g.ctx_rows));
+                    constexpr double kStaleUpdates = 32.0;
                     auto scale_of = [&](double q) {
-                        const double p = 1.0 - std::pow(1.0 - std::min(q, 1.0), static_cast<double>(h.flush_centers));
-                        return static_cast<float>(1.0 / std::max(1.0, p * g.blocks));
+                        q = std::min(std::max(q, 0.0), 1.0);
+                        const double p = 1.0 - std::pow(1.0 - q, static_cast<double>(h.flush_centers));
+                        const double avg = 1.0 / std::max(1.0, p * g.blocks);
+                        const double stale = kStaleUpdates / std::max(1e-30, g.blocks * q * h.flush_centers);
+                        return static_cast<float>(std::min(1.0, std::max(avg, stale)));
                     };
                     for (int32_t r = 0; r < g.cache_rows; ++r)
                         sc[static_cast<size_t>(r)] =
@@ -905,7 +921,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                     s->row_scale.upload(sc.data(), sc.size(), s->stream);
                     s->scale_blocks = g.blocks;
                     s->scale_flush = h.flush_centers;
-                    s->scale_rows = g.cache_rows * 4096 + g.ctx_rows;
+                    s->scale_rows = static_cast<int64_t>(g.cache_rows) * 4096 + g.ctx_rows;
                 }
                 h.row_scale = s->row_scale.p;
             }
@@ -929,6 +945,9 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             out.train_launches = 1;
             out.other_launches = sub_launches;
             out.cached_rows = g.cache_rows;
+            out.smem_rows = g.smem_rows;
+            out.floor_rows = floor_rows;
+            out.flush_centers = h.flush_centers;
             out.worker_warps = g.warps;
             out.ctx_batch = g.ctx_batch;
             out.blocks = g.blocks;

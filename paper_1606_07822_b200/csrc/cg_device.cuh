@@ -92,23 +92,73 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
 }
 
 __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); }
+
+// ---- packed fp32 (sm_100: FFMA2 / FADD2 / FMUL2, two lanes of math per instruction) ----
+// A float4 lives in four consecutive registers, so .xy and .zw are aligned register pairs
+// and every float4 op below is two packed instructions. A scalar operand is broadcast
+// by the instruction itself (SASS `R.F32`), so no register pair has to be built for it.
+__device__ __forceinline__ float2 lo2(float4 a) { return make_float2(a.x, a.y); }
+__device__ __forceinline__ float2 hi2(float4 a) { return make_float2(a.z, a.w); }
+__device__ __forceinline__ float4 cat4(float2 l, float2 h) { return make_float4(l.x, l.y, h.x, h.y); }
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
-    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    return cat4(__fadd2_rn(lo2(a), lo2(b)), __fadd2_rn(hi2(a), hi2(b)));
 }
 // a + s*b
 __device__ __forceinline__ float4 axpy4(float s, float4 b, float4 a) {
-    return make_float4(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y), fmaf(s, b.z, a.z), fmaf(s, b.w, a.w));
+    const float2 ss = make_float2(s, s);
+    return cat4(__ffma2_rn(ss, lo2(b), lo2(a)), __ffma2_rn(ss, hi2(b), hi2(a)));
 }
 __device__ __forceinline__ float4 scale4(float s, float4 b) {
-    return make_float4(s * b.x, s * b.y, s * b.z, s * b.w);
+    const float2 ss = make_float2(s, s);
+    return cat4(__fmul2_rn(ss, lo2(b)), __fmul2_rn(ss, hi2(b)));
 }
-__device__ __forceinline__ float dot4(float4 a, float4 b, float acc) {
-    acc = fmaf(a.x, b.x, acc);
-    acc = fmaf(a.y, b.y, acc);
-    acc = fmaf(a.z, b.z, acc);
-    return fmaf(a.w, b.w, acc);
+// Partial dot product in two interleaved sums (even and odd components); the caller
+// adds .x + .y once per dot.
+__device__ __forceinline__ float2 dot4(float4 a, float4 b, float2 acc) {
+    acc = __ffma2_rn(lo2(a), lo2(b), acc);
+    return __ffma2_rn(hi2(a), hi2(b), acc);
 }
 __device__ __forceinline__ bool nonzero4(float4 a) { return a.x != 0.f || a.y != 0.f || a.z != 0.f || a.w != 0.f; }
+
+// ---- atomics, bulk copies and mbarriers ----------------------------------------
+// Reads a 16-byte vector and leaves zeros in one atomic step (ATOMG.EXCH.128): drains
+// a delta row that other warps keep adding to with red.global without losing an add.
+__device__ __forceinline__ float4 atom_take4(float* p) {
+    unsigned long long lo, hi;
+    asm volatile(
+        "{\n\t.reg .b128 d, b;\n\tmov.b128 b, {%2, %2};\n\tatom.global.exch.b128 d, [%3], b;\n\t"
+        "mov.b128 {%0, %1}, d;\n\t}"
+        : "=l"(lo), "=l"(hi)
+        : "l"(0ull), "l"(p)
+        : "memory");
+    return make_float4(__uint_as_float(static_cast<unsigned>(lo)), __uint_as_float(static_cast<unsigned>(lo >> 32)),
+                       __uint_as_float(static_cast<unsigned>(hi)), __uint_as_float(static_cast<unsigned>(hi >> 32)));
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+// One arrival that also expects `bytes` of bulk-copy completions in this phase.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(
+            smem_u32(mb)),
+        "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy by the TMA unit (UBLKCP), completing on an mbarrier. Goes
+// through L2 like cp.async.cg: coherent with the red.global updates of other SMs.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* mb) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(mb))
+                 : "memory");
+}
+// Orders this thread's generic-proxy shared-memory writes before later bulk copies.
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---- warp transpose-reduce ---------------------------------------------------
 // p[0..N) are per-lane partial sums of N independent dot products (N a power of two,

@@ -96,9 +96,20 @@ int64_t sub_tiles(int64_t n);
 void launch_subsample(const SubArgs& a, cudaStream_t s, int* launches);
 
 // ---------------- throughput mode: Hogwild training (K1) ----------------------
+// The paper's per-worker node cache (NodeCache, trainer.hpp:75-138) becomes a per-CTA
+// cache of the top `cache_rows` syn1 rows (device rows [0, cache_rows): the
+// CacheSelection's rows lead the device row order), held in two tiers:
+//   * rows [0, smem_rows): deltas in shared memory, merged under per-row locks;
+//   * rows [smem_rows, cache_rows): deltas in a CTA-private slice of `tier2` (global
+//     memory, L2-resident for moderate K), merged with red.global.add and drained with
+//     an atomic exchange.
+// A warp reads a cached row as the base row plus its CTA's pending delta. Every
+// `flush_centers` merged centers the CTA drains the rows it touched into syn1, scaled
+// per row (row_scale: summing the deltas of rows few CTAs touch, averaging the CTA
+// replicas of rows many CTAs touch).
 struct HogArgs {
     float* syn0;               // [V * Dp]
-    float* syn1;               // [(V-1) * Dp], rows in usage-rank order
+    float* syn1;               // [V * Dp]: V-1 rows in device order + one all-zero pad row
     int32_t d4;                // Dp / 4 (row stride in float4)
     const int32_t* path_off;   // [V+1]
     const int32_t* path_code;  // (row << 1) | turn
@@ -109,42 +120,45 @@ struct HogArgs {
     float sig_scale;
     int32_t window;
     uint64_t win_key;
-    int32_t cache_rows;        // K rows cached in shared memory (rows [0, K))
+    int32_t cache_rows;        // K: syn1 rows [0, K) cached per CTA (both tiers)
+    int32_t smem_rows;         // S <= K: rows [0, S) in shared memory
+    float* tier2;              // [blocks][K - S][Dp] pending deltas of rows [S, K); all zero between launches
     int32_t ctx_cache_rows;    // syn0 rows [0, K0) -- the most frequent words -- cached per CTA too
     int32_t centers_per_warp;
-    int32_t cold_store;        // 1: plain stores for cold rows and syn0 (lossy Hogwild)
-    float hot_flush_scale;     // multiplier on block-cache deltas at flush (if row_scale == nullptr)
-    const float* row_scale;    // per cached row flush multiplier (syn1 rows, then syn0 rows), or nullptr
-    int32_t flush_centers;     // centers merged into a block cache between flushes
-    int32_t dummy_row;         // an all-zero syn1 row that pads cold-step groups
+    float hot_flush_scale;     // multiplier on cached deltas at flush (if row_scale == nullptr)
+    const float* row_scale;    // per cached row flush multiplier (syn1 rows [0, K), then syn0 rows), or nullptr
+    int32_t flush_centers;     // centers merged into a CTA's cache between flushes
+    int32_t dummy_row;         // the all-zero syn1 pad row
     int32_t ctx_batch;         // context rows staged per warp (<= 2 * window)
-    int32_t flusher;           // v4: 1 = the block's last warp is a cache flusher (set by the launcher)
-    int32_t probe;             // experiments only: 1 skip cold-row updates, 2 skip syn0 updates, 4 skip cache merges
+    int32_t flusher;           // 1 = the block's last warp is a cache flusher (set by the launcher)
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
 struct HogGeometry {
-    int warps;      // per block
-    int blocks;     // grid
-    int cpw;        // centers per warp per tile
-    int cache_rows;
-    int ctx_batch;  // contexts staged per warp
-    int variant;    // DCH
-    int kernel;     // 4 = hog4_kernel (default), 3 = hog_kernel
-    bool specialise;  // v4: use the row-width-specialised instantiation when there is one
-    bool flusher;     // v4: one extra (flusher) warp; only when registers leave room for it
-    int ctx_rows;     // v4: cached syn0 rows (most frequent context words)
+    int warps;        // worker warps per block
+    int blocks;       // grid
+    int cpw;          // centers per ticket
+    int cache_rows;   // K (both tiers)
+    int smem_rows;    // S
+    int ctx_batch;    // contexts staged per warp
+    int variant;      // float4 chunks per lane (1..3); 0 = the generic kernel (D > 384 or depth > 64)
+    bool specialise;  // use the row-width-specialised instantiation when there is one
+    bool flusher;     // one extra (flusher) warp; only when registers leave room for it
+    int ctx_rows;     // cached syn0 rows (most frequent context words)
     size_t smem;
 };
-// Depth limit on cached hot rows for this row width (none for the row-major kernel).
-int hog_hmax(int d4);
-// Picks the kernel variant for d4 and the launch geometry for the device.
 // Most frequent words whose syn0 rows K1 caches per CTA (averaged at flush, like the hot
 // syn1 rows): thousands of warps otherwise add stale updates to them at once.
 constexpr int kCtxCacheRows = 16;
-// Warps per CTA the registers allow for this row width (v4).
-int hog_max_warps(int d4);
-HogGeometry hog_plan(int d4, int cache_rows_wanted, int blocks_override, int warps_override, int cpw_override,
-                     int rows_override, int window, int kernel, int64_t tokens, int ctx_rows);
+// Longest Huffman path the row-group kernel stages per warp; deeper trees (and rows
+// wider than 384 floats) train on the generic kernel.
+constexpr int kMaxGroupDepth = 64;
+// Upper bound on the cached rows per CTA (touched-row bitmap in shared memory).
+constexpr int kMaxCacheRows = 16384;
+// Warps per CTA the registers allow for this row width / depth.
+int hog_max_warps(int d4, int max_depth);
+// Picks the kernel variant and the launch geometry for the device. smem_rows < 0 = default.
+HogGeometry hog_plan(int d4, int max_depth, int cache_rows, int smem_rows, int blocks_override, int warps_override,
+                     int cpw_override, int window, int64_t tokens, int ctx_rows);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 // ---------------- evaluation (cg_eval.cu) -----------------------------------------

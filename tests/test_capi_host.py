@@ -36,7 +36,7 @@ def test_library_exports_every_declared_symbol():
     for n in names:
         assert hasattr(lib, n), n
     assert set(names) == set(_lib.exported_symbols())
-    assert lib.cg_abi_version() == 2
+    assert lib.cg_abi_version() == 3
 
 
 def test_host_helpers_match_oracle():

@@ -121,30 +121,131 @@ def test_hogwild_planted_cluster_recall_matches_reference():
 
 
 # Every K1 instantiation: the row-width-specialised ones (D 100/128/200/300) and the
-# generic ones of each float4-chunk count (D 16/180/260), with the flusher warp (C2/C5
-# geometry) and with inline flushes (probe bit 4). Each must cover the stream and learn:
-# at least 90% of the loss reduction of the reference's own single-stream training on
-# the same corpus (the deterministic path, which is bit-identical to the reference).
-@pytest.mark.parametrize("dim,window,probe", [(100, 5, 0), (128, 5, 0), (200, 5, 0), (300, 5, 0), (300, 10, 0),
-                                              (16, 5, 0), (180, 5, 0), (260, 5, 0), (200, 5, 16), (200, 5, 32),
-                                              (300, 5, 48)])
-def test_hogwild_every_kernel_variant_learns(dim, window, probe):
-    c = CorpusConfig("variants", 300_000, 5000, 1.0, dim, window, 1e-3, 1, 11)
-    vocab, ids = vocab_from_raw(generate(c), 1, c.vocab)
-    tree, sel = setup(vocab)
-    base = dict(dim=dim, window=window, min_count=1, sample=c.sample, iterations=1, cache_nodes=31, seed=11)
-    det = api.train(ids, vocab, tree, sel, api.TrainConfig(**base, mode="deterministic"))
+# generic-width ones of each float4-chunk count (D 16/180/260), the generic kernel for rows
+# wider than 384 floats (D 512), and the cache layouts: every cached row in the L2 tier
+# (smem_rows 0), every one in shared memory, K = 256 (mostly L2 tier) and a flush after
+# every merged center. Each must cover the stream and learn: at least 90% of the loss
+# reduction of the reference's own single-stream training on the same 1M-token corpus (the
+# deterministic path, which is bit-identical to the reference).
+_VARIANT_CORPUS = {}
+
+
+def _variant_corpus():
+    if not _VARIANT_CORPUS:
+        c = CorpusConfig("variants", 1_000_000, 10000, 1.0, 100, 5, 1e-3, 1, 11)
+        vocab, ids = vocab_from_raw(generate(c), 1, c.vocab)
+        _VARIANT_CORPUS.update(c=c, vocab=vocab, ids=ids, det={})
+    return _VARIANT_CORPUS
+
+
+@pytest.mark.parametrize("dim,window,k,tune", [
+    (100, 5, 31, {}), (128, 5, 31, {}), (200, 5, 31, {}), (300, 5, 31, {}), (300, 10, 31, {}),
+    (16, 5, 31, {}), (180, 5, 31, {}), (260, 5, 31, {}), (512, 5, 31, {}),
+    (200, 5, 31, dict(smem_rows=0)), (200, 5, 31, dict(smem_rows=31)), (300, 5, 256, {}),
+    (100, 5, 256, {}), (200, 5, 31, dict(flush_centers=1)), (512, 5, 256, dict(flush_centers=1))])
+def test_hogwild_every_kernel_variant_learns(dim, window, k, tune):
+    vc = _variant_corpus()
+    c, vocab, ids = vc["c"], vc["vocab"], vc["ids"]
+    c = CorpusConfig("variants", c.tokens, c.vocab, c.zipf_s, dim, window, c.sample, 1, c.seed)
+    tree, sel = setup(vocab, k)
+    base = dict(dim=dim, window=window, min_count=1, sample=c.sample, iterations=1, cache_nodes=k, seed=11)
+    key = (dim, window, k)
+    if key not in vc["det"]:
+        det = api.train(ids, vocab, tree, sel, api.TrainConfig(**base, mode="deterministic"))
+        init = api.init_model(vocab.size(), dim, 11)
+        vc["det"][key] = (_loss(init, tree, vocab, ids, c), _loss(det, tree, vocab, ids, c))
+    li, ld = vc["det"][key]
     s = api.Session(vocab, tree, sel, api.TrainConfig(**base, mode="hogwild"))
-    s.tune(probe=probe)
+    s.tune(**tune)
     s.upload_ids(ids)
     e = s.train_range(0, 0, ids.size, 0, 1)
     m = s.download()
     s.close()
     assert e.words == ids.size and e.pairs > 0
+    assert e.cached_rows >= k, (e.cached_rows, k)  # K is honoured (plus the stability floor)
     assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
-    init = api.init_model(vocab.size(), dim, 11)
-    li, ld, lh = (_loss(x, tree, vocab, ids, c) for x in (init, det, m))
-    assert li - lh > 0.9 * (li - ld), (lh, ld, li, e.worker_warps, e.ctx_batch, e.cached_rows)
+    lh = _loss(m, tree, vocab, ids, c)
+    assert li - lh > 0.9 * (li - ld), (lh, ld, li, e.worker_warps, e.ctx_batch, e.cached_rows, e.smem_rows)
+
+
+def test_hogwild_honours_k_and_u():
+    """cache_nodes = K sets the cached rows (both tiers), flush_interval = u the flush
+    period (u x worker warps merged centers per CTA); the stability floor only adds rows
+    when K is below it, and min_cache_rows < 0 honours even K = 0 literally."""
+    c, vocab, ids = c1()
+    got = {}
+    for k, u, floor in [(0, 10, 0), (0, 10, -1), (31, 10, 0), (64, 3, 0), (1024, 1, 0)]:
+        tree, sel = setup(vocab, k)
+        cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=1,
+                              cache_nodes=k, flush_interval=u, seed=1, mode="hogwild")
+        s = api.Session(vocab, tree, sel, cfg)
+        s.tune(min_cache_rows=floor)
+        s.upload_ids(ids[:200_000])
+        e = s.train_range(0, 0, 200_000, 0, 1)
+        s.close()
+        got[(k, u, floor)] = e
+        assert e.flush_centers == u * e.worker_warps, (e.flush_centers, u, e.worker_warps)
+        assert e.smem_rows == min(8, e.cached_rows)
+    assert got[(0, 10, -1)].cached_rows == 0 and got[(0, 10, -1)].floor_rows == 0
+    fl = got[(0, 10, 0)].floor_rows
+    assert 1 <= fl <= 64 and got[(0, 10, 0)].cached_rows == fl
+    assert got[(31, 10, 0)].cached_rows == max(31, fl)
+    assert got[(64, 3, 0)].cached_rows == 64
+    assert got[(1024, 1, 0)].cached_rows == 1024
+
+
+def test_hogwild_flusher_shutdown_stress():
+    """200 launches with a flusher warp (D 200, W 5: 11 workers + flusher) and a flush
+    request after every merged center: the flusher's shutdown must never hang."""
+    c = CorpusConfig("flush-stress", 40_000, 2000, 1.0, 200, 5, 1e-3, 1, 13)
+    vocab, ids = vocab_from_raw(generate(c), 1, c.vocab)
+    tree, sel = setup(vocab, 31)
+    cfg = api.TrainConfig(dim=200, window=5, min_count=1, sample=1e-3, iterations=1, cache_nodes=31, seed=13,
+                          mode="hogwild")
+    s = api.Session(vocab, tree, sel, cfg)
+    s.tune(flush_centers=1)
+    s.upload_ids(ids)
+    for ep in range(200):
+        e = s.train_range(ep, 0, ids.size, 0, 1)
+        assert e.words == ids.size
+    m = s.download()
+    s.close()
+    assert np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all()
+
+
+def test_hogwild_rows_beyond_32bit_offsets():
+    """V x Dp >= 2^31 floats (V 7.2M, D 300: syn0 alone is 8.7 GB). Training a small
+    stream that includes the highest ids must update exactly the rows it touches: with
+    32-bit row offsets the writes of ids >= 7.06M would land in other rows."""
+    import torch
+
+    V, D = 7_200_000, 300
+    counts = np.maximum(1, (1e9 / np.arange(1, V + 1)).astype(np.int64))
+    vocab = api.Vocabulary(counts)
+    tree, sel = setup(vocab, 31)
+    rng = np.random.default_rng(5)
+    hi_ids = np.arange(V - 2000, V, dtype=np.int32)
+    ids = np.concatenate([rng.integers(0, 50_000, 100_000).astype(np.int32), np.repeat(hi_ids, 5)])
+    rng.shuffle(ids)
+    cfg = api.TrainConfig(dim=D, window=5, min_count=1, sample=0.0, iterations=1, cache_nodes=31, seed=5,
+                          mode="hogwild")
+    s = api.Session(vocab, tree, sel, cfg)
+    s.upload_ids(ids)
+    m_dev = s.model_tensor()
+    Dp = (D + 7) // 8 * 8
+    syn0 = m_dev[: V * Dp].view(V, Dp)
+    probe_rows = torch.tensor(np.r_[np.arange(60_000, 60_100), np.arange(V - 5000, V - 4900)], device=syn0.device)
+    before = syn0[probe_rows].clone()
+    hi_before = syn0[torch.tensor(hi_ids, device=syn0.device).long()].clone()
+    e = s.train_range(0, 0, ids.size, 0, 1)
+    torch.cuda.synchronize()
+    assert e.words == ids.size
+    # rows no token touches (ids 60000.., V-5000..) are bit-identical; the high ids moved
+    assert torch.equal(syn0[probe_rows], before)
+    moved = (syn0[torch.tensor(hi_ids, device=syn0.device).long()] != hi_before).any(dim=1)
+    assert bool(moved.all())
+    assert bool(torch.isfinite(syn0[torch.tensor(hi_ids, device=syn0.device).long()]).all())
+    s.close()
 
 
 def test_hogwild_without_subsampling_matches_reference_c1():
