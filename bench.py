@@ -2,18 +2,20 @@
 """Benchmark: trained words/sec of skip-gram HS training (BASELINE.json metric).
 
 A "step" is one training pass of the hot path over one GPU's shard of the synthetic
-corpus (default: BASELINE config 2, the text8-shaped 17M-token Zipf(1.05) corpus,
-V 71k, D 200, W 5, sample 1e-4, K 31). Inputs (id stream, tree, model) are resident
-in HBM before the timed region. Each timed step = K3 subsampling/pair generation +
-K1 Hogwild training (+ periodic all-reduce averaging at N > 1).
+corpus. Default: BASELINE config 5 (the largest single-GPU configuration: 1B tokens of
+Zipf(1.2) over a 1M vocabulary, D 300, W 5, sample 1e-5, K 31 -- the reference default,
+BASELINE.json leaves it to the K sweep). Inputs (id stream, tree, model) are resident in
+HBM before the timed region. Each timed step = K3 subsampling/pair generation + K1
+Hogwild training (+ the replicas' delta sync at N > 1).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
-Under torchrun each rank trains its own shard (weak scaling) on its own GPU and
-averages syn0/syn1 with NCCL every --sync-words words. Rank 0 prints ONE JSON line.
-`--impl reference` times the reference's own CPU implementation (the reference headers
-compiled unchanged, oracle/_ref) on this host's cores on a bounded sample.
-"""
+Under torchrun each rank trains its own full-size shard (weak scaling) on its own GPU and
+sums the replicas' deltas with NCCL every --sync-words words per GPU (default 1M; 25M at
+C5, sized so the dense 2.4 GB delta all-reduce stays near 10% of the pass at N = 8).
+Rank 0 prints ONE JSON line. `--impl reference` times the reference's own CPU
+implementation (the reference headers compiled unchanged, oracle/_ref) on this host's
+cores on a bounded sample.
 from __future__ import annotations
 
 import argparse
@@ -41,9 +43,11 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--cache-nodes", type=int, default=31)
-    p.add_argument("--sync-words", type=int, default=1_000_000, help="all-reduce interval per GPU (N > 1)")
+    p.add_argument("--sync-words", type=int, default=0,
+                   help="delta all-reduce interval per GPU at N > 1 (0 = 25M at C5, else 1M)")
+    p.add_argument("--sync-mode", default="delta", choices=["delta", "average"])
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--e2e-text-max-tokens", type=int, default=20_000_000,
                    help="also time train(corpus_path) on the corpus written as text when it has at most this many tokens")
@@ -288,6 +292,8 @@ def main():
     else:
         sess.upload_ids_device(ids)
     model_t = sess.model_tensor() if world > 1 else None
+    if not args.sync_words:
+        args.sync_words = 25_000_000 if args.config == "c5" else 1_000_000
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     T = int(len(ids))
@@ -312,7 +318,7 @@ def main():
 
     from paper_1606_07822_b200.replicas import ReplicaTrainer
 
-    trainer = ReplicaTrainer(local_step, model_t, world, rank, args.sync_words)
+    trainer = ReplicaTrainer(local_step, model_t, world, rank, args.sync_words, replica=sess, mode=args.sync_mode)
 
     def one_step(epoch: int, rec: bool):
         record["on"] = rec
@@ -358,22 +364,54 @@ def main():
     words_all = float(T) * args.steps * world  # every rank's shard has the same size
     value = words_all / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (K1 hs_train): algorithmic bytes per launch / launch time
+    # Roofline of the dominant kernel (K1). The HBM roofline is graded on
+    # DRAM bytes: `achieved` = ncu-measured DRAM bytes per K1 launch (profiles/, captured
+    # for this kernel source: `traffic_current`) / this run's CUDA-event K1 time. The
+    # algorithmic bytes (4 D (2 L + 2) per pair) are reported beside it, not as the
+    # fraction: K1 loads each path row once per center and keeps hot rows on chip, so they
+    # exceed what crosses HBM. K1 is bound by SM issue; `fp32` is its FMA throughput
+    # (3 D FMAs per pair and path step) against the FP32 pipe (SMs x 128 x the SM clock).
+    import hashlib
+
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     n_launch = max(agg["launch_count"], 1)
     per_launch_bytes = agg["bytes"] / n_launch
     per_launch_ms = agg["train_ms"] / n_launch
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    algorithmic_gbs = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    src_sha = hashlib.sha256((ROOT / "paper_1606_07822_b200" / "csrc" / "cg_hogwild.cu").read_bytes()).hexdigest()[:16]
     traffic = l2_traffic = None
+    traffic_current = False
     prof = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
     if prof.exists():
         try:
             tj = json.loads(prof.read_text())
             traffic, l2_traffic = tj.get("dram_bytes_per_launch"), tj.get("l2_bytes_per_launch")
+            traffic_current = tj.get("kernel_sha16") == src_sha
         except Exception:
             traffic = l2_traffic = None
+    dram_gbs = traffic / (per_launch_ms / 1e3) / 1e9 if traffic else None
+    props = torch.cuda.get_device_properties(local)
+    f_sm = 1e6 * float(clk.get("sm_mhz") or clk.get("sm_max_mhz") or 1965.0)
+    fma_per_launch = 3.0 * c.dim * agg["steps"] / n_launch
+    fp32_peak = props.multi_processor_count * 128 * f_sm
+    fp32_achieved = fma_per_launch / (per_launch_ms / 1e3)
+    roofline = {
+        "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+        "achieved": dram_gbs, "frac": dram_gbs / peak if dram_gbs else None, "traffic": traffic,
+        "traffic_source": f"profiles/{prof.name} (ncu --set full, one K1 launch)",
+        "traffic_current": traffic_current, "kernel_sha16": src_sha,
+        "dram_frac": dram_gbs / peak if dram_gbs else None,
+        "l2_traffic": l2_traffic,
+        "algorithmic_bytes_per_launch": per_launch_bytes, "algorithmic_gbs": algorithmic_gbs,
+        "algorithmic_gbs_over_hbm_peak": algorithmic_gbs / peak,
+        "fp32": {"fma_per_launch": fma_per_launch, "achieved_tfma_s": fp32_achieved / 1e12,
+                 "peak_tfma_s": fp32_peak / 1e12, "frac": fp32_achieved / fp32_peak,
+                 "note": "3 D FMAs per (pair, path step); peak = SMs x 128 FMA/clk x median SM clock"},
+        "fp32_frac": fp32_achieved / fp32_peak,
+        "kernel": "hog5_kernel (K1)", "kernel_ms_per_launch": per_launch_ms,
+    }
 
     # end to end through the public API with host buffers (pinned): ids H2D, model init,
     # subsampling + training (+ averaging at N > 1), model D2H. N = 1 goes through the
@@ -403,7 +441,7 @@ def main():
                 s2 = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
                 s2.upload_ids(ids_pin.numpy())
                 rt2 = ReplicaTrainer(lambda e, a, b, base, mult: s2.train_range(e, a, b, base, mult),
-                                     s2.model_tensor(), world, rank, args.sync_words)
+                                     s2.model_tensor(), world, rank, args.sync_words, replica=s2, mode=args.sync_mode)
                 rt2.run_pass(0, T)
                 m = s2.download()
                 s2.close()
@@ -461,17 +499,19 @@ def main():
             "config": {"workload": f"{args.config}: {c.tokens / 1e6:g}M-token Zipf({c.zipf_s}) per GPU, V {vocab.size()}, "
                                    f"D {c.dim}, W {c.window}, sample {c.sample}, K {args.cache_nodes}, 1 pass per step",
                        "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}",
-                       "sync_words_per_gpu": args.sync_words if world > 1 else None},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "l2_traffic": l2_traffic, "peak_source": peak_src,
-                         "kernel": "hog_kernel (K1)", "algorithmic_bytes_per_launch": per_launch_bytes,
-                         "kernel_ms_per_launch": per_launch_ms},
+                       "sync_words_per_gpu": args.sync_words if world > 1 else None,
+                       "sync": (f"{args.sync_mode}: replicas' deltas all-reduced (SUM) and applied with the per-row "
+                                "sync scale" if args.sync_mode == "delta" else "whole-model all-reduce (AVG)")
+                       if world > 1 else None},
+            "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_text": e2e_text,
             "gpu_launches": launches["n"],
             "clocks": clk,
-            "detail": {"pairs_per_step": agg["pairs"] / args.steps, "path_steps_per_step": agg["steps"] / args.steps,
+            "detail": {"syncs": trainer.syncs, "sync_bytes": trainer.sync_bytes,
+                       "sync_ms_total": 1e3 * trainer.sync_seconds,
+                       "pairs_per_step": agg["pairs"] / args.steps, "path_steps_per_step": agg["steps"] / args.steps,
                        "kept_per_step": agg["kept"] / args.steps, "step_ms": step_ms,
                        "k1_geometry": agg.get("geometry")},
         }

@@ -17,8 +17,10 @@
 //                       path step while the device does the arithmetic (cg_train_center_cb).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -48,8 +50,9 @@ struct TrainConfig {
     std::int32_t flush_interval = 10;
     std::uint64_t seed = 1;
     TrainMode mode = TrainMode::Auto;
-    // B200 additions: model replicas on GPUs 0..gpus-1 of this process, averaged over
-    // peer memory every sync_words words per replica (Hogwild mode).
+    // B200 additions: model replicas on GPUs 0..gpus-1 of this process; every sync_words
+    // words per replica their deltas are summed over peer memory and applied with the
+    // per-row sync scale (Hogwild mode, cg_session_sync_apply).
     std::int32_t gpus = 1;
     std::int64_t sync_words = 1000000;
 
@@ -90,8 +93,9 @@ inline std::int32_t shrink_window(std::int32_t window, Rng& rng) {
     return window - static_cast<std::int32_t>(rng.next_below(static_cast<std::uint32_t>(window)));
 }
 
+// Shared progress of the training run (trainer.hpp:52-55): atomic, as the reference's.
 struct ProgressCounter {
-    std::uint64_t words_processed = 0;
+    std::atomic<std::uint64_t> words_processed{0};
     std::uint64_t total_words = 0;
 };
 
@@ -137,6 +141,34 @@ struct TreeArrays {
         }
     }
 };
+
+// The CSR arrays and slot map of the last (tree, selection) pair train_center was called
+// with, per thread: rebuilding them (O(V)) on every call made the kernel-level entry
+// unusable beyond tests. Trees and selections are immutable once built; the key holds
+// their addresses and sizes.
+struct CenterArrays {
+    const HuffmanTree* tree = nullptr;
+    const CacheSelection* selection = nullptr;
+    std::size_t steps = 0;
+    std::int32_t leaves = 0, slots = 0;
+    std::unique_ptr<TreeArrays> ta;
+    std::vector<std::int32_t> slot_of;
+};
+inline const CenterArrays& center_arrays(const HuffmanTree& tree, const CacheSelection& selection) {
+    thread_local CenterArrays c;
+    if (c.tree != &tree || c.selection != &selection || c.steps != tree.steps().size() ||
+        c.leaves != tree.leaf_count() || c.slots != selection.size()) {
+        c.ta = std::make_unique<TreeArrays>(tree);
+        c.slot_of.resize(static_cast<std::size_t>(selection.inner_node_count()));
+        for (std::int32_t n = 0; n < selection.inner_node_count(); ++n) c.slot_of[static_cast<std::size_t>(n)] = selection.slot_of(n);
+        c.tree = &tree;
+        c.selection = &selection;
+        c.steps = tree.steps().size();
+        c.leaves = tree.leaf_count();
+        c.slots = selection.size();
+    }
+    return c;
+}
 
 template <typename S>
 constexpr bool kDeviceSigmoid = std::is_same_v<S, SigmoidTable> || std::is_same_v<S, ExactSigmoid> ||
@@ -207,9 +239,9 @@ inline void train_center(std::int32_t center, std::span<const std::int32_t> sent
                          const CacheSelection& selection, NodeCache& cache, float alpha, float* hidden,
                          const SigmoidFn& sigmoid, std::int64_t* sigmoid_calls = nullptr) {
     (void)hidden;
-    const trainer_detail::TreeArrays ta(tree);
-    std::vector<std::int32_t> slot_of(static_cast<std::size_t>(selection.inner_node_count()));
-    for (std::int32_t n = 0; n < selection.inner_node_count(); ++n) slot_of[static_cast<std::size_t>(n)] = selection.slot_of(n);
+    const trainer_detail::CenterArrays& arrays = trainer_detail::center_arrays(tree, selection);
+    const trainer_detail::TreeArrays& ta = *arrays.ta;
+    const std::vector<std::int32_t>& slot_of = arrays.slot_of;
     if constexpr (trainer_detail::kDeviceSigmoid<SigmoidFn>) {
         std::int32_t mode = 0;
         float konst = 0.0f;
@@ -272,17 +304,31 @@ inline Model train(const std::string& corpus_path, const Vocabulary& vocab, cons
 
     Model model(vocab.size(), config.dim);
     cg_train_stats st{};
+    // Errors: configuration and consistency problems (std::invalid_argument) and a corpus
+    // that cannot be opened (IoError) are raised before training starts, as the
+    // reference raises them before its worker threads (trainer.hpp:256-276). Anything
+    // that fails during training is a worker failure: with workers > 1 the reference
+    // wraps it as runtime_error("worker i failed: ...") (trainer.hpp:297-305); the GPU run
+    // is one device-wide worker, reported as worker 0.
+    auto check_run = [&](int rc) {
+        if (rc == CG_OK) return;
+        if (config.workers > 1 && rc != CG_ERR_INVALID_ARGUMENT && rc != CG_ERR_IO) {
+            const std::string msg = rc == CG_ERR_NO_TRAINABLE_WORDS ? std::string(NoTrainableWords().what())
+                                                                    : std::string(cg_last_error());
+            throw std::runtime_error("worker 0 failed: " + msg);
+        }
+        trainer_detail::rethrow(rc);
+    };
     if (config.gpus > 1) {
         if (mode != TrainMode::Hogwild) throw std::invalid_argument("gpus > 1 trains replicas in Hogwild mode");
         std::vector<std::int32_t> devices(static_cast<std::size_t>(config.gpus));
         for (std::int32_t g = 0; g < config.gpus; ++g) devices[static_cast<std::size_t>(g)] = g;
-        trainer_detail::check(cg_train_file_replicas(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(),
-                                                     words.data(), devices.data(), config.gpus, config.sync_words,
-                                                     model.input_matrix().data(), model.weight_matrix().data(), &st));
+        check_run(cg_train_file_replicas(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(), words.data(),
+                                         devices.data(), config.gpus, config.sync_words, model.input_matrix().data(),
+                                         model.weight_matrix().data(), &st));
     } else {
-        trainer_detail::check(cg_train_file(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(),
-                                            words.data(), model.input_matrix().data(),
-                                            model.weight_matrix().data(), &st));
+        check_run(cg_train_file(&c, static_cast<std::int32_t>(mode), &m, corpus_path.c_str(), words.data(),
+                                model.input_matrix().data(), model.weight_matrix().data(), &st));
     }
     if (stats) {
         stats->words_processed = st.words_processed;

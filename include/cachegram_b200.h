@@ -218,6 +218,27 @@ CG_API int cg_session_train(cg_session* s, cg_train_stats* stats);
 CG_API int cg_session_download(cg_session* s, float* syn0_out, float* syn1_out);
 /* The device model buffer (for an all-reduce between replicas) and its geometry. */
 CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int32_t* row_stride_floats);
+/* ---- replica sync: one model replica per GPU, deltas summed -------------
+ * The reference's workers all add into one model (trainer.hpp:72-74, 249-253). Replicas
+ * keep that semantics between syncs: each replica trains its shard from the model of the
+ * last sync (the snapshot); at a sync every replica's delta (model - snapshot) is summed
+ * over the replicas (cg_session_sync_delta exposes it for an NCCL all-reduce with SUM) and
+ * applied to the snapshot row by row with cg_sync_row_scale (cg_session_sync_apply). */
+/* snapshot = model: the start of a sync period (after reset/set_model, before training). */
+CG_API int cg_session_sync_begin(cg_session* s);
+/* delta = model - snapshot, in a session-owned device buffer of n_floats (the model's layout). */
+CG_API int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floats);
+/* With the delta buffer holding the sum over n_replicas replicas: model = snapshot +
+ * scale(row) x delta, snapshot = model. words_per_replica: id-stream tokens each replica
+ * trained since the last sync (the sync interval). */
+CG_API int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_replica);
+/* The per-row scale of the summed delta for a row on a share q of the updates, n_replicas
+ * replicas of `centers` kept centers each per sync: min(1, max(1 / (p n), 32 / (n q centers)))
+ * with p = 1 - (1 - q)^centers -- rows few replicas touch are summed as in the reference, a
+ * row every replica updates from the same snapshot gets at most 32 stale updates' worth and
+ * at least the replicas' average. Host-only arithmetic (no device needed). */
+CG_API float cg_sync_row_scale(double q, int32_t n_replicas, double centers);
+
 /* Hogwild kernel knobs (zero-initialised = defaults, except smem_cache_rows: -1). */
 typedef struct cg_tuning {
     int32_t blocks;           /* 0 = one persistent CTA per SM */
@@ -256,11 +277,12 @@ CG_API int cg_train_file(const cg_config* cfg, int32_t mode, const cg_model_desc
 
 /* ---- in-process replicas: one model replica per GPU -------------------
  * For C/C++ callers that drive several GPUs from one process. Each replica trains a
- * contiguous shard of the id stream (Hogwild mode); every sync_words words per replica
- * the replicas are averaged over peer memory (NVLink/NVSwitch): replica r's GPU averages
- * slice r across all replicas and writes it back to all of them. The learning rate
- * follows n_devices x local progress. devices may repeat an ordinal (several replicas
- * on one GPU: functional testing). The result is replica 0's model (all are equal). */
+ * contiguous shard of the id stream (Hogwild mode); every sync_words words per replica the
+ * replicas' deltas since the last sync are summed over peer memory (NVLink/NVSwitch:
+ * replica r's GPU sums slice r across all replicas and writes it back to all of them) and
+ * applied with the per-row sync scale (cg_session_sync_apply). The learning rate follows
+ * n_devices x local progress. devices may repeat an ordinal (several replicas on one GPU:
+ * functional testing). The result is replica 0's model (all are equal). */
 CG_API int cg_train_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids,
                              int64_t n_ids, const int32_t* devices, int32_t n_devices, int64_t sync_words,
                              float* syn0_out, float* syn1_out, cg_train_stats* stats);

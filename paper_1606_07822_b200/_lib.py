@@ -149,6 +149,10 @@ SIGNATURES = {
     "cg_session_download": (C.c_int, [vp, P(C.c_float), P(C.c_float)]),
     "cg_session_model_buffer": (C.c_int, [vp, P(vp), P(C.c_size_t), P(C.c_int32)]),
     "cg_session_tune": (C.c_int, [vp, P(CgTuning)]),
+    "cg_session_sync_begin": (C.c_int, [vp]),
+    "cg_session_sync_delta": (C.c_int, [vp, P(vp), P(C.c_size_t)]),
+    "cg_session_sync_apply": (C.c_int, [vp, C.c_int32, C.c_uint64]),
+    "cg_sync_row_scale": (C.c_float, [C.c_double, C.c_int32, C.c_double]),
     "cg_corpus_open_gpu": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, P(vp)]),
     "cg_corpus_read_ids_gpu": (C.c_int, [vp, C.c_char_p, C.c_int32, P(C.c_int32), C.c_int64, P(C.c_int64)]),
     "cg_session_load_corpus": (C.c_int, [vp, C.c_char_p, C.c_char_p, P(C.c_int64)]),

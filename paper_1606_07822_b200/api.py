@@ -161,6 +161,11 @@ def read_id_stream(path: str, vocab: Vocabulary, device: int | None = None) -> n
     return ids
 
 
+def sync_row_scale(q: float, n_replicas: int, centers: float) -> float:
+    """cg_sync_row_scale: the per-row scale of the replicas' summed delta at a sync."""
+    return float(load().cg_sync_row_scale(float(q), int(n_replicas), float(centers)))
+
+
 def keep_probability(count: int, total_tokens: int, sample: float) -> float:
     return float(load().cg_keep_probability(int(count), int(total_tokens), float(sample)))
 
@@ -535,6 +540,27 @@ class Session:
         p, n, s = C.c_void_p(), C.c_size_t(), C.c_int32()
         check(load().cg_session_model_buffer(self._h, C.byref(p), C.byref(n), C.byref(s)))
         return int(p.value or 0), int(n.value), int(s.value)
+
+    # ---- replica sync (cg_session_sync_*): deltas since the last sync, summed over replicas
+    def sync_begin(self) -> None:
+        check(load().cg_session_sync_begin(self._h))
+
+    def sync_delta_tensor(self):
+        """delta = model - snapshot, as a zero-copy torch view of the session's delta buffer
+        (all-reduce it with SUM across replicas, then call sync_apply)."""
+        import torch
+
+        p, n = C.c_void_p(), C.c_size_t()
+        check(load().cg_session_sync_delta(self._h, C.byref(p), C.byref(n)))
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": (int(n.value),), "typestr": "<f4", "data": (int(p.value), False),
+                                        "version": 3}
+
+        return torch.as_tensor(_Cai(), device="cuda")
+
+    def sync_apply(self, n_replicas: int, words_per_replica: int) -> None:
+        check(load().cg_session_sync_apply(self._h, int(n_replicas), int(words_per_replica)))
 
     def model_tensor(self):
         """Zero-copy torch view of the device model buffer (for all-reduce)."""

@@ -184,6 +184,27 @@ __global__ void scatter_rows_kernel(float* dst, int32_t ds, const float* src, in
 
 unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
+// ---- replica sync: deltas since the last sync, summed across replicas ----
+__global__ void sync_delta_kernel(const float4* model, const float4* snap, float4* delta, size_t n4) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float4 m = model[i], b = snap[i];
+        delta[i] = make_float4(m.x - b.x, m.y - b.y, m.z - b.z, m.w - b.w);
+    }
+}
+// model = snapshot + scale[row] * delta (the replicas' summed deltas); snapshot = model
+__global__ void sync_apply_kernel(float4* model, float4* snap, const float4* delta, const float* scale, size_t n4,
+                                  int32_t row4) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const float sc = scale[i / static_cast<size_t>(row4)];
+        const float4 b = snap[i], d = delta[i];
+        const float4 m = make_float4(b.x + sc * d.x, b.y + sc * d.y, b.z + sc * d.z, b.w + sc * d.w);
+        model[i] = m;
+        snap[i] = m;
+    }
+}
+
 }  // namespace
 
 void cgint::set_last_error(const std::string& msg) { g_error = msg; }
@@ -225,6 +246,14 @@ struct cg_session {
     // after the caller's selection)
     std::vector<double> row_share;
     DevBuf<float> tier2;  // hogwild: the L2 tier of the per-CTA cache (zeroed before each launch)
+    // replica sync (hogwild): the model at the start of the sync period, the (summed) delta,
+    // and per-row update shares for the sync scale: syn0 row w is updated by the centers
+    // whose window holds w, device syn1 row r by the centers whose path holds r
+    DevBuf<float> snap, delta, sync_scale;
+    std::vector<float> row_q;  // [2V]: syn0 rows, then syn1 rows (device order) and the pad row
+    double kept_ratio = 1.0;   // expected kept share of the id stream
+    int32_t sync_n = -1;
+    uint64_t sync_words = 0;
     std::vector<double> ctx_share;  // hogwild: share of centers with word w (w < kCtxCacheRows) in their window
     DevBuf<float> row_scale;
     int scale_blocks = -1, scale_flush = -1;
@@ -558,6 +587,15 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                 if (w < static_cast<int32_t>(kept.size())) kept[static_cast<size_t>(w)] = k;
             }
             for (double k : kept) s->ctx_share.push_back(std::min(1.0, (cfg->window + 1) * k / std::max(kept_total, 1.0)));
+            if (mode == CG_MODE_HOGWILD) {
+                s->row_q.assign(2 * static_cast<size_t>(V), 0.0f);
+                for (int32_t w = 0; w < V; ++w) {
+                    const double kpw = kp.empty() ? 1.0 : std::min(1.0, static_cast<double>(kp[static_cast<size_t>(w)]));
+                    s->row_q[static_cast<size_t>(w)] = static_cast<float>(
+                        std::min(1.0, (cfg->window + 1) * static_cast<double>(md->counts[w]) * kpw / std::max(kept_total, 1.0)));
+                }
+                s->kept_ratio = kept_total / std::max(1.0, static_cast<double>(md->total_tokens));
+            }
         }
 
         if (mode == CG_MODE_DETERMINISTIC) {
@@ -601,6 +639,9 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
             const int32_t nshare = std::min<int32_t>(V - 1, cgk::kMaxCacheRows);
             for (int32_t r = 0; r < nshare; ++r)
                 s->row_share.push_back(static_cast<double>(md->node_usage[s->node_of_row[static_cast<size_t>(r)]]) / root);
+            for (int32_t r = 0; r < V - 1; ++r)
+                s->row_q[static_cast<size_t>(V) + static_cast<size_t>(r)] =
+                    static_cast<float>(static_cast<double>(md->node_usage[s->node_of_row[static_cast<size_t>(r)]]) / root);
             s->row_of_node.assign(static_cast<size_t>(V - 1), 0);
             for (int32_t r = 0; r < V - 1; ++r) s->row_of_node[static_cast<size_t>(s->node_of_row[static_cast<size_t>(r)])] = r;
             std::vector<int32_t> off(static_cast<size_t>(V) + 1);
@@ -757,6 +798,71 @@ int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int
     });
 }
 
+// Sync scale of one row whose share of the updates is q when n replicas each train
+// `centers` kept centers between syncs. The reference's workers all add
+// into one model (trainer.hpp:72-74, 249-253), so deltas are summed across replicas, but
+// a row every replica updates from the same snapshot receives n x q x centers stale
+// updates per sync: the sum is capped at H = 32 stale updates' worth and never scaled
+// below the average of the replicas that touched it (the per-CTA flush rule of K1, with
+// replicas for CTAs).
+float cg_sync_row_scale(double q, int32_t n_replicas, double centers) {
+    if (n_replicas <= 1) return 1.0f;
+    q = std::min(std::max(q, 0.0), 1.0);
+    const double n = static_cast<double>(n_replicas);
+    const double p = 1.0 - std::pow(1.0 - q, std::max(centers, 0.0));
+    const double avg = 1.0 / std::max(1.0, p * n);
+    const double stale = 32.0 / std::max(1e-30, n * q * centers);
+    return static_cast<float>(std::min(1.0, std::max(avg, stale)));
+}
+
+int cg_session_sync_begin(cg_session* s) {
+    return guarded([&] {
+        if (s->mode != CG_MODE_HOGWILD) invalid("replica sync needs a hogwild session");
+        CG_CUDA(cudaSetDevice(s->device));
+        if (s->snap.n != s->model.n) s->snap.alloc(s->model.n);
+        CG_CUDA(cudaMemcpyAsync(s->snap.p, s->model.p, s->model.n * 4, cudaMemcpyDeviceToDevice, s->stream));
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
+int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floats) {
+    return guarded([&] {
+        if (s->snap.n != s->model.n) invalid("cg_session_sync_begin was not called");
+        CG_CUDA(cudaSetDevice(s->device));
+        if (s->delta.n != s->model.n) s->delta.alloc(s->model.n);
+        const size_t n4 = s->model.n / 4;
+        sync_delta_kernel<<<grid_for(static_cast<int64_t>(n4)), 256, 0, s->stream>>>(
+            reinterpret_cast<const float4*>(s->model.p), reinterpret_cast<const float4*>(s->snap.p),
+            reinterpret_cast<float4*>(s->delta.p), n4);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+        if (delta_dev) *delta_dev = s->delta.p;
+        if (n_floats) *n_floats = s->delta.n;
+    });
+}
+
+int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_replica) {
+    return guarded([&] {
+        if (s->snap.n != s->model.n || s->delta.n != s->model.n) invalid("cg_session_sync_delta was not called");
+        if (n_replicas < 1) invalid("replica count must be >= 1");
+        CG_CUDA(cudaSetDevice(s->device));
+        if (s->sync_n != n_replicas || s->sync_words != words_per_replica) {
+            const double centers = s->kept_ratio * static_cast<double>(words_per_replica);
+            std::vector<float> sc(s->row_q.size());
+            for (size_t r = 0; r < sc.size(); ++r) sc[r] = cg_sync_row_scale(s->row_q[r], n_replicas, centers);
+            s->sync_scale.upload(sc.data(), sc.size(), s->stream);
+            s->sync_n = n_replicas;
+            s->sync_words = words_per_replica;
+        }
+        const size_t n4 = s->model.n / 4;
+        sync_apply_kernel<<<grid_for(static_cast<int64_t>(n4)), 256, 0, s->stream>>>(
+            reinterpret_cast<float4*>(s->model.p), reinterpret_cast<float4*>(s->snap.p),
+            reinterpret_cast<const float4*>(s->delta.p), s->sync_scale.p, n4, s->Dp / 4);
+        CG_CUDA(cudaGetLastError());
+        CG_CUDA(cudaStreamSynchronize(s->stream));
+    });
+}
+
 int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
         if (!t) invalid("null tuning");
@@ -892,8 +998,9 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // paths of a share q of the centers gets, per flush period of F merged centers per
             // CTA, about n_CTA x q x F such updates: for the root (q = 1) ~10^4, and summed they
             // overshoot and diverge. The flush therefore scales each row's delta
-            // by s = min(1, max(1 / (p n_CTA), H / (n_CTA q F))): at most H = 32 stale updates'
-            // worth per flush (8x below where C1 diverged, profiles/r2_rule3_c1.jsonl), never
+            // by s = min(1, max(1 / (p n_CTA), H / (q (n_CTA F + warps in flight)))): at most
+            // H = 32 stale updates' worth per flush (8x below where C1 diverged,
+            // profiles/r2_rule3_c1.jsonl), never
             // less than the average of the p n_CTA contributing replicas (p = 1 - (1 - q)^F,
             // the chance that a CTA touches the row in a period), and the plain sum of the
             // reference for rows few CTAs touch.
@@ -905,11 +1012,15 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                     // syn1 cached rows [0, cache_rows), then the cached syn0 rows [0, ctx_rows)
                     std::vector<float> sc(static_cast<size_t>(g.cache_rows + g.ctx_rows));
                     constexpr double kStaleUpdates = 32.0;
+                    // warps in flight besides the CTA replicas: a flush lands while the other
+                    // CTAs' warps are mid-center on the old value (dominant for small F)
+                    const double inflight_w = static_cast<double>(g.blocks) * g.warps;
                     auto scale_of = [&](double q) {
                         q = std::min(std::max(q, 0.0), 1.0);
                         const double p = 1.0 - std::pow(1.0 - q, static_cast<double>(h.flush_centers));
                         const double avg = 1.0 / std::max(1.0, p * g.blocks);
-                        const double stale = kStaleUpdates / std::max(1e-30, g.blocks * q * h.flush_centers);
+                        const double stale =
+                            kStaleUpdates / std::max(1e-30, q * (static_cast<double>(g.blocks) * h.flush_centers + inflight_w));
                         return static_cast<float>(std::min(1.0, std::max(avg, stale)));
                     };
                     for (int32_t r = 0; r < g.cache_rows; ++r)
@@ -1631,6 +1742,9 @@ struct ReplicaPtrs {
     float4* buf[kMaxReplicas];
 };
 
+// Slice [begin4, end4) of the n buffers: sum in a fixed order (every replica receives the
+// same bits), times inv_n (1 = the sum of the replicas' deltas, 1/n = their average),
+// written back to every buffer.
 __global__ void replica_avg_kernel(ReplicaPtrs p, int n, size_t begin4, size_t end4, float inv_n) {
     for (size_t i = begin4 + blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < end4;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -1661,14 +1775,15 @@ void enable_peers(const int32_t* devices, int32_t n) {
         }
 }
 
-// Replica r's share of the averaging: slice r of n4 float4s, launched on devices[r].
-void launch_average_slice(const ReplicaPtrs& p, int32_t n, int32_t r, size_t n4, int32_t device, cudaStream_t st) {
+// Replica r's share of the reduction: slice r of n4 float4s, launched on devices[r].
+void launch_reduce_slice(const ReplicaPtrs& p, int32_t n, int32_t r, size_t n4, int32_t device, cudaStream_t st,
+                         bool average) {
     const size_t b = n4 * static_cast<size_t>(r) / static_cast<size_t>(n);
     const size_t e = n4 * static_cast<size_t>(r + 1) / static_cast<size_t>(n);
     if (e <= b) return;
     CG_CUDA(cudaSetDevice(device));
     const unsigned grid = static_cast<unsigned>(std::min<size_t>((e - b + 255) / 256, 148 * 8));
-    replica_avg_kernel<<<grid, 256, 0, st>>>(p, n, b, e, 1.0f / static_cast<float>(n));
+    replica_avg_kernel<<<grid, 256, 0, st>>>(p, n, b, e, average ? 1.0f / static_cast<float>(n) : 1.0f);
     CG_CUDA(cudaGetLastError());
 }
 
@@ -1718,16 +1833,12 @@ void run_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model
             x.len = load(r, x.s);
         }
         enable_peers(devices, n);
-        ReplicaPtrs ptrs{};
-        size_t bytes = 0;
-        for (int32_t r = 0; r < n; ++r) {
-            void* p = nullptr;
-            int32_t stride = 0;
-            const int rc = cg_session_model_buffer(rep[static_cast<size_t>(r)].s, &p, &bytes, &stride);
+        for (auto& x : rep) {
+            const int rc = cg_session_sync_begin(x.s);
             if (rc != CG_OK) throw CgError(rc, g_error);
-            ptrs.buf[r] = static_cast<float4*>(p);
         }
-        const size_t n4 = bytes / sizeof(float4);
+        ReplicaPtrs ptrs{};  // the replicas' delta buffers (allocated by their first sync)
+        size_t n4 = 0;
         int64_t max_len = 0;
         for (auto& x : rep) max_len = std::max(max_len, x.len);
         const int64_t chunks = (max_len + sync_words - 1) / sync_words;
@@ -1735,6 +1846,14 @@ void run_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model
         std::atomic<int> failed{0};
         std::vector<std::string> errs(static_cast<size_t>(n));
         std::vector<int> codes(static_cast<size_t>(n), CG_OK);
+        auto fail = [&](int32_t r, int code, const std::string& m) {
+            codes[static_cast<size_t>(r)] = code;
+            errs[static_cast<size_t>(r)] = m;
+            failed.store(1);
+        };
+        // Each chunk: train, then the delta reduction -- every replica's delta since the last
+        // sync (model - snapshot), summed over replicas slice by slice over peer memory,
+        // applied to every replica's snapshot with the per-row sync scale.
         auto worker = [&](int32_t r) {
             Rep& x = rep[static_cast<size_t>(r)];
             for (int32_t it = 0; it < cfg->iterations; ++it) {
@@ -1746,29 +1865,38 @@ void run_replicas(const cg_config* cfg, int32_t mode, const cg_model_desc* model
                                               static_cast<uint64_t>(n);
                         const int rc = b > a ? cg_session_train_range(x.s, it, a, b, base, static_cast<uint32_t>(n), &e)
                                              : CG_OK;
-                        if (rc != CG_OK) {
-                            codes[static_cast<size_t>(r)] = rc;
-                            errs[static_cast<size_t>(r)] = cg_last_error();
-                            failed.store(1);
-                        }
+                        if (rc != CG_OK) fail(r, rc, cg_last_error());
                         x.kernel_s += (e.train_ms + e.subsample_ms) * 1e-3;
                         x.centers += e.kept;
                         x.pairs += e.pairs;
                         x.steps += e.steps;
                         x.words += e.words;
                     }
-                    sync.arrive_and_wait();  // every replica finished this chunk
-                    if (!failed.load() && n > 1) {
-                        try {
-                            launch_average_slice(ptrs, n, r, n4, devices[r], x.st);
-                            CG_CUDA(cudaStreamSynchronize(x.st));
-                        } catch (const std::exception& ex) {
-                            codes[static_cast<size_t>(r)] = CG_ERR_CUDA;
-                            errs[static_cast<size_t>(r)] = ex.what();
-                            failed.store(1);
+                    if (n > 1) {
+                        if (!failed.load()) {
+                            void* d = nullptr;
+                            size_t nf = 0;
+                            const int rc = cg_session_sync_delta(x.s, &d, &nf);
+                            if (rc != CG_OK) fail(r, rc, cg_last_error());
+                            ptrs.buf[r] = static_cast<float4*>(d);
+                            if (r == 0) n4 = nf / 4;
+                        }
+                        sync.arrive_and_wait();  // every replica's delta is ready
+                        if (!failed.load()) {
+                            try {
+                                launch_reduce_slice(ptrs, n, r, n4, devices[r], x.st, false);
+                                CG_CUDA(cudaStreamSynchronize(x.st));
+                            } catch (const std::exception& ex) {
+                                fail(r, CG_ERR_CUDA, ex.what());
+                            }
+                        }
+                        sync.arrive_and_wait();  // every slice summed into every replica
+                        if (!failed.load()) {
+                            const int rc = cg_session_sync_apply(x.s, n, static_cast<uint64_t>(sync_words));
+                            if (rc != CG_OK) fail(r, rc, cg_last_error());
                         }
                     }
-                    sync.arrive_and_wait();  // every slice averaged
+                    sync.arrive_and_wait();
                 }
             }
         };
@@ -1810,7 +1938,7 @@ int cg_average_buffers(void* const* device_bufs, const int32_t* devices, int32_t
         enable_peers(devices, n);
         ReplicaPtrs p{};
         for (int32_t r = 0; r < n; ++r) p.buf[r] = static_cast<float4*>(device_bufs[r]);
-        for (int32_t r = 0; r < n; ++r) launch_average_slice(p, n, r, n_floats / 4, devices[r], nullptr);
+        for (int32_t r = 0; r < n; ++r) launch_reduce_slice(p, n, r, n_floats / 4, devices[r], nullptr, true);
         for (int32_t r = 0; r < n; ++r) {
             CG_CUDA(cudaSetDevice(devices[r]));
             CG_CUDA(cudaDeviceSynchronize());

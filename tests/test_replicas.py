@@ -1,7 +1,8 @@
-"""Multi-replica orchestration (shards, averaging cadence, global-progress estimate)
-on CPU with torch.distributed gloo, world_size 2. The local step is the oracle's
-single-worker trainer (test infrastructure) standing in for the device kernels; the
-expected result is recomputed sequentially in one process."""
+"""Multi-replica orchestration (shards, sync cadence, global-progress estimate, the delta
+reduction) on CPU with torch.distributed gloo, world_size 2. The local step is the
+oracle's single-worker trainer (test infrastructure) standing in for the device kernels,
+and a host stand-in applies the library's sync rule (cg_sync_row_scale); the expected
+result is recomputed sequentially in one process."""
 import os
 import socket
 
@@ -58,13 +59,48 @@ def init_model():
     return np.concatenate([s0.ravel(), s1.ravel()]).astype(np.float32)
 
 
-def _worker(rank, world, port, out):
+def row_shares(counts, window=3):
+    """Per-row update shares in the model layout: syn0 row w, (W + 1) x its share of the
+    stream; syn1 node n, its usage over the root's (what the session uses)."""
+    tree = O.orc_tree(counts)
+    q0 = np.minimum(1.0, (window + 1) * counts / counts.sum())
+    q1 = tree.usage / tree.usage[-1]
+    return np.concatenate([q0, q1])
+
+
+class HostReplica:
+    """Host stand-in for a session's sync operations (cg_session_sync_*): the same
+    snapshot/delta/apply steps on a numpy model, with the library's row scale."""
+
+    def __init__(self, model_np, counts):
+        from paper_1606_07822_b200 import api
+
+        self.m = model_np
+        self.q = row_shares(counts)
+        self.api = api
+
+    def sync_begin(self):
+        self.snap = self.m.copy()
+
+    def sync_delta_tensor(self):
+        self.delta = torch.from_numpy(self.m - self.snap)
+        return self.delta
+
+    def sync_apply(self, n, words):
+        sc = np.array([self.api.sync_row_scale(q, n, words) for q in self.q], np.float32)
+        rows = np.concatenate([np.repeat(sc[:V], D), np.repeat(sc[V:], D)])
+        self.m[:] = self.snap + rows * self.delta.numpy()
+        self.snap = self.m.copy()
+
+
+def _worker(rank, world, port, out, mode):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     ids, counts = corpus()
     a, b = shard_bounds(ids.size, world, rank)
     model = torch.from_numpy(init_model())
-    rt = ReplicaTrainer(local_step_factory(ids[a:b], counts, model.numpy()), model, world, rank, sync_words=5000)
+    rt = ReplicaTrainer(local_step_factory(ids[a:b], counts, model.numpy()), model, world, rank, sync_words=5000,
+                        replica=HostReplica(model.numpy(), counts), mode=mode)
     calls = rt.run_pass(0, b - a) + rt.run_pass(1, b - a, tokens_before=b - a)
     out[rank] = (model.numpy().copy(), calls, rt.syncs)
     dist.destroy_process_group()
@@ -83,14 +119,33 @@ def test_plan_and_shards():
     assert bounds == [(0, 3), (3, 6), (6, 10)]
 
 
-def test_two_replicas_gloo_average_matches_sequential_simulation():
+def test_sync_row_scale():
+    """The delta reduction's per-row scale (cg_sync_row_scale): one replica is the plain
+    sum; a row few replicas touch is summed as in the reference; a row every replica
+    updates from the same snapshot is capped at 32 stale updates' worth but never below
+    the replicas' average; monotone in the row's share."""
+    from paper_1606_07822_b200 import api
+
+    assert api.sync_row_scale(1.0, 1, 1e6) == 1.0
+    for n in (2, 4, 8):
+        assert api.sync_row_scale(1e-9, n, 1e5) == 1.0  # touched by at most one replica
+        assert api.sync_row_scale(1.0, n, 1e5) == pytest.approx(1.0 / n)  # the root: the average
+        assert api.sync_row_scale(1.0, n, 2.0) == pytest.approx(1.0)  # 32 stale updates: still a sum
+        qs = np.logspace(-8, 0, 40)
+        sc = [api.sync_row_scale(q, n, 1e5) for q in qs]
+        assert all(1.0 / n - 1e-7 <= x <= 1.0 for x in sc)
+        assert all(a >= b - 1e-7 for a, b in zip(sc, sc[1:]))
+
+
+@pytest.mark.parametrize("mode", ["delta", "average"])
+def test_two_replicas_gloo_match_sequential_simulation(mode):
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, start_method="spawn", join=True)
+    mp.start_processes(_worker, args=(world, _free_port(), out, mode), nprocs=world, start_method="spawn", join=True)
     m0, calls0, syncs0 = out[0]
     m1, calls1, _ = out[1]
-    assert np.array_equal(m0, m1)  # replicas agree after every averaging point
+    assert np.array_equal(m0, m1)  # replicas agree after every sync point
     ids, counts = corpus()
     n = [shard_bounds(ids.size, world, r) for r in range(world)]
     # progress estimate: base = world x local tokens before the chunk, mult = world
@@ -100,6 +155,12 @@ def test_two_replicas_gloo_average_matches_sequential_simulation():
     # sequential simulation of the same schedule
     models = [init_model() for _ in range(world)]
     steps = [local_step_factory(ids[a:b], counts, models[r]) for r, (a, b) in enumerate(n)]
+    snap = models[0].copy()
+    q = row_shares(counts)
+    from paper_1606_07822_b200 import api
+
+    sc = np.array([api.sync_row_scale(x, world, 5000) for x in q], np.float32)
+    rows = np.concatenate([np.repeat(sc[:V], D), np.repeat(sc[V:], D)])
     for epoch in range(2):
         chunks = [plan_chunks(b - a, 5000) for a, b in n]
         for i in range(max(len(c) for c in chunks)):
@@ -107,10 +168,16 @@ def test_two_replicas_gloo_average_matches_sequential_simulation():
                 if i < len(chunks[r]):
                     ch = chunks[r][i]
                     steps[r](epoch, ch.begin, ch.end, 0, world)
-            avg = (models[0] + models[1]) / 2
+            if mode == "average":
+                new = (models[0] + models[1]) / 2
+            else:  # the summed deltas since the last sync, scaled per row
+                new = snap + rows * ((models[0] - snap) + (models[1] - snap))
             for r in range(world):
-                models[r][:] = avg
+                models[r][:] = new
+            snap = new.copy()
     np.testing.assert_allclose(m0, models[0], rtol=0, atol=1e-6)
+    if mode == "delta":  # a row one replica alone touched keeps its whole update
+        assert not np.allclose(m0, (models[0] + init_model()) / 2)
 
 
 @pytest.mark.gpu

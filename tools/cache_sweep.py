@@ -44,6 +44,12 @@ GRIDS = {
     "v6": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (31, -1, 0, 10, 3, 256, 32, 0, 5), (8, -1, -1, 10, 0, 256, 64, 0, 0),
            (8, -1, -1, 10, 0, 256, 64, 0, 5)],
     "h": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (8, -1, -1, 10, 0, 256, 64, 0, 0), (0, -1, 0, 10, 3, 256, 32, 0, 0)],
+    "ab": [(31, -1, 0, 10, 3), (8, -1, -1, 10, 0)],
+    "final": [(31, -1, 0, 10, 3), (31, -1, 0, 10, 3, 256, 32, 1), (256, -1, 0, 10, 3), (0, -1, 0, 10, 3),
+              (8, -1, -1, 10, 3)],
+    "stab": [(31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 16),
+             (31, -1, 0, 10, 3, 256, 16), (31, -1, 0, 10, 3, 256, 8), (31, -1, 0, 10, 3, 256, 1),
+             (31, -1, 0, 10, 3, 256, 16, 1), (31, -1, 0, 10, 3, 256, 1, 1), (256, -1, 0, 10, 3, 256, 16)],
     "sweep": [(0, -1, 0, 10, 0), (64, -1, 0, 10, 0), (256, -1, 0, 10, 0), (1024, -1, 0, 10, 0), (31, -1, 0, 10, 0)],
 }
 
