@@ -16,6 +16,7 @@ C5, sized so the dense 2.4 GB delta all-reduce stays near 10% of the pass at N =
 Rank 0 prints ONE JSON line. `--impl reference` times the reference's own CPU
 implementation (the reference headers compiled unchanged, oracle/_ref) on this host's
 cores on a bounded sample.
+"""
 from __future__ import annotations
 
 import argparse
@@ -227,6 +228,26 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
+def cpu_topology() -> dict:
+    """Host threads this process may use and the machine's physical cores (psutil), so a
+    CPU number says whether its threads were hardware threads or cores."""
+    info = {"threads_available": cpu_threads(), "logical_cpus": os.cpu_count()}
+    try:
+        import psutil
+
+        info["physical_cores"] = psutil.cpu_count(logical=False)
+    except Exception:
+        info["physical_cores"] = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
+
+
 def auto_sample(c) -> int:
     """Tokens per reference pass: about 10-30 s of CPU work on a 16-32 core host."""
     return {"c1": 1_000_000, "c2": 17_000_000, "c3": 20_000_000, "c4": 6_000_000, "c5": 20_000_000}[c.name]
@@ -255,7 +276,7 @@ def main():
             "config": {"workload": f"{args.config}: {c.tokens // 10**6}M-token Zipf({c.zipf_s}) V {vocab.size()} "
                                    f"D {c.dim} W {c.window} sample {c.sample} K {args.cache_nodes}",
                        "sample_tokens_per_step": n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "host": cpu_topology(),
                              "sample": f"first {n} tokens of the {args.config} corpus, 1 pass per step, "
                                        f"reference train() with workers={threads}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -485,6 +506,7 @@ def main():
             sample = args.cpu_sample_tokens or auto_sample(c)
             rates, walls, n = run_reference(c, vocab, ids, threads, sample, 1, args.cache_nodes)
             cpu = {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference",
+                   "host": cpu_topology(),
                    "sample": f"first {n} tokens of the {args.config} corpus, 1 pass, reference train() "
                              f"(headers compiled unchanged, -O3) with workers={threads}"}
         except Exception as ex:  # reported, not fatal

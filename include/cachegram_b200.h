@@ -254,6 +254,8 @@ typedef struct cg_tuning {
                                  K is smaller; > 0 = at least this many rows; < 0 = none, K is honoured
                                  literally (K = 0 then diverges on small vocabularies at full-GPU
                                  concurrency) */
+    int32_t kernel;           /* 0 = default; 5 = v5 (packed FP32 FMA, two-tier cache); 7 = v7 (each center's
+                                 products on the tensor cores, mma.sync TF32) */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 

@@ -99,7 +99,7 @@ class CgEpochStats(C.Structure):
 class CgTuning(C.Structure):
     _fields_ = [("blocks", C.c_int32), ("warps_per_block", C.c_int32), ("centers_per_warp", C.c_int32),
                 ("smem_cache_rows", C.c_int32), ("hot_flush_scale", C.c_float), ("flush_centers", C.c_int32),
-                ("min_cache_rows", C.c_int32)]
+                ("min_cache_rows", C.c_int32), ("kernel", C.c_int32)]
 
 
 P = C.POINTER

@@ -511,10 +511,11 @@ class Session:
                                           ptr(np.ascontiguousarray(model.syn1), C.c_float)))
 
     def tune(self, blocks: int = 0, warps: int = 0, centers_per_warp: int = 0, smem_rows: int = -1,
-             hot_flush_scale: float = 0.0, flush_centers: int = 0, min_cache_rows: int = 0) -> None:
+             hot_flush_scale: float = 0.0, flush_centers: int = 0, min_cache_rows: int = 0, kernel: int = 0) -> None:
         """Hogwild kernel knobs (cg_tuning): smem_rows = cached rows held in shared memory
         (-1: 8); min_cache_rows = stability floor (0 auto, > 0 at least, < 0 none)."""
-        t = _lib.CgTuning(blocks, warps, centers_per_warp, smem_rows, hot_flush_scale, flush_centers, min_cache_rows)
+        t = _lib.CgTuning(blocks, warps, centers_per_warp, smem_rows, hot_flush_scale, flush_centers, min_cache_rows,
+                          kernel)
         check(load().cg_session_tune(self._h, C.byref(t)))
 
     def train_range(self, epoch: int, begin: int, end: int, progress_base: int = 0,

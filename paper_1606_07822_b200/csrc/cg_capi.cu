@@ -240,7 +240,7 @@ struct cg_session {
     DevBuf<uint32_t> tile_count;
     DevBuf<uint64_t> tile_off;
     DevBuf<unsigned long long> counters;
-    cg_tuning tune{0, 0, 0, -1, 0.0f, 0, 0};
+    cg_tuning tune{0, 0, 0, -1, 0.0f, 0, 0, 0};
     // hogwild: share of the paths through device row r (usage / root usage), for the first
     // min(V-1, kMaxCacheRows) rows (the cacheable ones; device rows are in usage order
     // after the caller's selection)
@@ -811,7 +811,8 @@ float cg_sync_row_scale(double q, int32_t n_replicas, double centers) {
     const double n = static_cast<double>(n_replicas);
     const double p = 1.0 - std::pow(1.0 - q, std::max(centers, 0.0));
     const double avg = 1.0 / std::max(1.0, p * n);
-    const double stale = 32.0 / std::max(1e-30, n * q * centers);
+    static const double H = std::getenv("CG_SYNC_H") ? std::atof(std::getenv("CG_SYNC_H")) : 32.0;
+    const double stale = H / std::max(1e-30, n * q * centers);
     return static_cast<float>(std::min(1.0, std::max(avg, stale)));
 }
 
@@ -867,6 +868,7 @@ int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
         if (!t) invalid("null tuning");
         if (t->smem_cache_rows > cgk::kMaxCacheRows) invalid("smem_cache_rows out of range");
+        if (t->kernel != 0 && t->kernel != 5 && t->kernel != 7) invalid("kernel must be 0, 5 or 7");
         s->tune = *t;
     });
 }
@@ -953,7 +955,13 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
             const int blocks = s->tune.blocks > 0 ? s->tune.blocks : sms;
-            const double inflight = static_cast<double>(blocks) * cgk::hog_max_warps(s->Dp / 4, s->max_depth);
+            // K1 version: v7 (tensor cores) or v5; the warps in flight set the stability floor
+            cgk::HogGeometry g{};
+            bool v7 = s->tune.kernel == 7 &&
+                      cgk::hog7_plan(s->Dp / 4, std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0, blocks,
+                                     s->tune.warps_per_block, s->tune.centers_per_warp, n, s->max_depth, &g);
+            const double inflight =
+                static_cast<double>(blocks) * (v7 ? g.warps : cgk::hog_max_warps(s->Dp / 4, s->max_depth));
             int32_t floor_rows = 0;
             if (s->tune.min_cache_rows == 0) {
                 for (int32_t r = 0; r < static_cast<int32_t>(s->row_share.size()); ++r)
@@ -973,9 +981,12 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                    s->ctx_share[static_cast<size_t>(ctx_rows)] * inflight >= kHotUpdaters)
                 ++ctx_rows;
             h.dummy_row = s->V - 1;
-            const cgk::HogGeometry g = cgk::hog_plan(h.d4, s->max_depth, want_rows, s->tune.smem_cache_rows, s->tune.blocks,
-                                                     s->tune.warps_per_block, s->tune.centers_per_warp, s->cfg.window, n,
-                                                     ctx_rows);
+            if (v7)
+                v7 = cgk::hog7_plan(s->Dp / 4, want_rows, ctx_rows, blocks, s->tune.warps_per_block,
+                                    s->tune.centers_per_warp, n, s->max_depth, &g);
+            if (!v7)
+                g = cgk::hog_plan(h.d4, s->max_depth, want_rows, s->tune.smem_cache_rows, s->tune.blocks,
+                                  s->tune.warps_per_block, s->tune.centers_per_warp, s->cfg.window, n, ctx_rows);
             if (g.smem == 0) invalid("dim too large for the generic kernel's shared-memory row buffers");
             // flush_interval u (trainer.hpp:127): each worker warp flushes every u of its
             // centers in the reference; here a CTA's workers share one cache, so it is
@@ -985,7 +996,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // The L2 tier: rows [S, K) of every CTA's cache, zeroed before each launch (the
             // kernel leaves it zero; re-zeroing keeps an aborted launch from leaking deltas).
             const size_t t2n = static_cast<size_t>(g.blocks) *
-                               static_cast<size_t>(g.cache_rows - g.smem_rows) * s->Dp;
+                               static_cast<size_t>(g.cache_rows - g.smem_rows + (g.variant == 7 ? g.ctx_rows : 0)) * s->Dp;
             h.tier2 = nullptr;
             if (t2n > 0) {
                 if (s->tier2.n < t2n) s->tier2.alloc(t2n);

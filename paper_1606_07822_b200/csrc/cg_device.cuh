@@ -100,6 +100,10 @@ __device__ __forceinline__ float4 f4(float a) { return make_float4(a, a, a, a); 
 __device__ __forceinline__ float2 lo2(float4 a) { return make_float2(a.x, a.y); }
 __device__ __forceinline__ float2 hi2(float4 a) { return make_float2(a.z, a.w); }
 __device__ __forceinline__ float4 cat4(float2 l, float2 h) { return make_float4(l.x, l.y, h.x, h.y); }
+#ifndef CG_FFMA2
+#define CG_FFMA2 1  // 0: scalar FFMA/FADD (same results up to rounding order; experiments: tools/ab_build.py)
+#endif
+#if CG_FFMA2
 __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     return cat4(__fadd2_rn(lo2(a), lo2(b)), __fadd2_rn(hi2(a), hi2(b)));
 }
@@ -118,6 +122,20 @@ __device__ __forceinline__ float2 dot4(float4 a, float4 b, float2 acc) {
     acc = __ffma2_rn(lo2(a), lo2(b), acc);
     return __ffma2_rn(hi2(a), hi2(b), acc);
 }
+#else
+__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+__device__ __forceinline__ float4 axpy4(float s, float4 b, float4 a) {
+    return make_float4(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y), fmaf(s, b.z, a.z), fmaf(s, b.w, a.w));
+}
+__device__ __forceinline__ float4 scale4(float s, float4 b) { return make_float4(s * b.x, s * b.y, s * b.z, s * b.w); }
+__device__ __forceinline__ float2 dot4(float4 a, float4 b, float2 acc) {
+    acc.x = fmaf(a.x, b.x, acc.x);
+    acc.x = fmaf(a.y, b.y, acc.x);
+    acc.x = fmaf(a.z, b.z, acc.x);
+    acc.x = fmaf(a.w, b.w, acc.x);
+    return acc;
+}
+#endif
 __device__ __forceinline__ bool nonzero4(float4 a) { return a.x != 0.f || a.y != 0.f || a.z != 0.f || a.w != 0.f; }
 
 // ---- atomics, bulk copies and mbarriers ----------------------------------------

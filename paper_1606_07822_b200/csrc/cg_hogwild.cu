@@ -30,6 +30,9 @@
 #ifndef CG_W2
 #define CG_W2 12  // warps per CTA the D <= 256 variant is compiled for (experiments: tools/ab_build.py)
 #endif
+#ifndef CG_T2_READ
+#define CG_T2_READ 1  // 1: warps read an L2-tier cached row as base + their CTA's pending delta; 0: base only
+#endif
 #ifndef CG_STAGE_BULK
 #define CG_STAGE_BULK 1  // 1: rows staged by bulk copies (TMA unit, UBLKCP); 0: cp.async (LDGSTS)
 #endif
@@ -546,7 +549,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog5_kernel(HogArgs a) {
                                 const int q = lane + 32 * k;
                                 if (in_row<DCH>(k, q, d4)) U[g][k] = add4(U[g][k], dblk[row[g] * d4 + q]);
                             }
-                        } else if (row[g] < K) {
+                        } else if (CG_T2_READ && row[g] < K) {
 #pragma unroll
                             for (int k = 0; k < DCH; ++k) {
                                 const int q = lane + 32 * k;
@@ -1034,6 +1037,7 @@ HogGeometry hog_plan(int d4, int max_depth, int cache_rows, int smem_rows, int b
 
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     switch (g.variant) {
+        case 7: launch_hog7(a, g, s); break;
         case 0: {
             auto k = hog_generic_kernel<kGenericWarps>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));

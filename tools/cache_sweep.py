@@ -50,6 +50,8 @@ GRIDS = {
     "stab": [(31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 16),
              (31, -1, 0, 10, 3, 256, 16), (31, -1, 0, 10, 3, 256, 8), (31, -1, 0, 10, 3, 256, 1),
              (31, -1, 0, 10, 3, 256, 16, 1), (31, -1, 0, 10, 3, 256, 1, 1), (256, -1, 0, 10, 3, 256, 16)],
+    "v7": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (31, -1, 0, 10, 3, 256, 32, 0, 7), (8, -1, -1, 10, 3, 256, 32, 0, 7),
+           (0, -1, 0, 10, 3, 256, 32, 0, 7)],
     "sweep": [(0, -1, 0, 10, 0), (64, -1, 0, 10, 0), (256, -1, 0, 10, 0), (1024, -1, 0, 10, 0), (31, -1, 0, 10, 0)],
 }
 
@@ -101,7 +103,7 @@ def main():
                               cache_nodes=k, flush_interval=u, seed=c.seed, mode="hogwild")
         sess = api.Session(vocab, tree, sel, cfg)
         kern = hot[3] if len(hot) > 3 else 0
-        sess.tune(smem_rows=srows, min_cache_rows=floor, flush_centers=hot[2] if len(hot) > 2 else 0)
+        sess.tune(smem_rows=srows, min_cache_rows=floor, flush_centers=hot[2] if len(hot) > 2 else 0, kernel=kern)
         if isinstance(ids, np.ndarray):
             sess.upload_ids(ids)
         else:

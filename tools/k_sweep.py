@@ -3,11 +3,11 @@
 {0, 64, 256, 1024} inner nodes").
 
 For each K, on one GPU:
-* K1 throughput: trained words/s of one full pass (K3 + K1, ids resident in HBM), with
-  the caller's K honoured exactly (`min_cache_rows = -1`: no minimum of 31 rows), and
-  the effective number of rows the per-CTA shared-memory cache holds (K is capped by
-  shared memory: 48 KB of rows per CTA, i.e. 40 rows at D 300, and by the depth limit of
-  the device row order -- cg_capi.cu, hog_plan in cg_hogwild.cu);
+* K1 throughput: trained words/s of one full pass (K3 + K1, ids resident in HBM). K is
+  honoured: every CTA caches the K CacheSelection rows (the hottest 8 in shared memory,
+  the rest as CTA-private delta rows in L2), plus the stability floor when K is below it
+  (`floor_rows`; cg_tuning.min_cache_rows), flushed every u x (worker warps) merged
+  centers (cg_capi.cu, hog_plan in cg_hogwild.cu);
 * HS log-loss of the trained model on 2^20 evaluation pairs (checker: the C oracle's
   formula of acceptance.cpp:100-110), against the untrained model's;
 * the reference's own train() (oracle/_ref, all host threads) with the same K on a
@@ -64,7 +64,6 @@ def main():
         cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
                               cache_nodes=k, seed=c.seed, mode="hogwild")
         sess = api.Session(vocab, tree, sel, cfg)
-        sess.tune(min_cache_rows=-1)
         if isinstance(ids, np.ndarray):
             sess.upload_ids(ids)
         else:
@@ -86,11 +85,13 @@ def main():
         finite = bool(np.isfinite(m.syn0).all() and np.isfinite(m.syn1).all())
         del m
         kmed = float(np.median(kms))
-        row = {"config": a.config, "k": k, "cached_rows_per_cta": e.cached_rows, "worker_warps": e.worker_warps,
+        row = {"config": a.config, "k": k, "cached_rows_per_cta": e.cached_rows, "smem_rows": e.smem_rows,
+               "l2_tier_rows": e.cached_rows - e.smem_rows, "floor_rows": e.floor_rows,
+               "flush_centers": e.flush_centers, "worker_warps": e.worker_warps,
                "ctx_batch": e.ctx_batch, "blocks": e.blocks, "tokens": T, "pairs": int(e.pairs), "steps": int(e.steps),
                "k1_ms": kmed, "pass_ms_wall": float(np.median(ms)), "words_per_s_k1": T / (kmed / 1e3),
                "words_per_s_pass": T / (float(np.median(ms)) / 1e3),
-               "roofline_achieved_gbs": 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs) / (kmed / 1e3) / 1e9,
+               "algorithmic_gbs": 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs) / (kmed / 1e3) / 1e9,
                "loss": loss, "loss_init": loss_init, "finite": finite, "eval_pairs": int(cen.size)}
         if a.ref_tokens > 0:
             rates, walls, n = bench.run_reference(c, vocab, ids, threads, a.ref_tokens, 1, k)

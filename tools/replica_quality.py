@@ -29,6 +29,7 @@ def main():
     p.add_argument("--n", type=int, nargs="+", default=[2, 4])
     p.add_argument("--sync", type=int, nargs="+", default=[100_000])
     p.add_argument("--pairs", type=int, default=1 << 20)
+    p.add_argument("--kernel", type=int, default=0)
     p.add_argument("--out", default="")
     a = p.parse_args()
     c = CONFIGS[a.config]
