@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--hot-flush-scale", type=float, default=0.0)
     p.add_argument("--flush-centers", type=int, default=0)
     p.add_argument("--min-cache-rows", type=int, default=0)
+    p.add_argument("--kernel", type=int, default=0, help="K1 version (0 = default)")
     return p.parse_args()
 
 
@@ -307,7 +308,7 @@ def main():
     stream = torch.cuda.current_stream()
     sess = api.Session(vocab, tree, sel, cfg, device=local, stream=stream.cuda_stream)
     sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.hot_flush_scale, args.flush_centers,
-              args.min_cache_rows)
+              args.min_cache_rows, args.kernel)
     if isinstance(ids, np.ndarray):
         sess.upload_ids(ids)
     else:
@@ -334,7 +335,7 @@ def main():
             agg["launch_count"] += e.train_launches
             agg["geometry"] = {"blocks": e.blocks, "worker_warps": e.worker_warps, "ctx_batch": e.ctx_batch,
                                "cached_rows_per_cta": e.cached_rows, "smem_rows": e.smem_rows,
-                               "floor_rows": e.floor_rows, "flush_centers": e.flush_centers}
+                               "floor_rows": e.floor_rows, "flush_centers": e.flush_centers, "kernel": e.kernel}
         return e
 
     from paper_1606_07822_b200.replicas import ReplicaTrainer
@@ -392,8 +393,6 @@ def main():
     # fraction: K1 loads each path row once per center and keeps hot rows on chip, so they
     # exceed what crosses HBM. K1 is bound by SM issue; `fp32` is its FMA throughput
     # (3 D FMAs per pair and path step) against the FP32 pipe (SMs x 128 x the SM clock).
-    import hashlib
-
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
@@ -401,7 +400,10 @@ def main():
     per_launch_bytes = agg["bytes"] / n_launch
     per_launch_ms = agg["train_ms"] / n_launch
     algorithmic_gbs = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    src_sha = hashlib.sha256((ROOT / "paper_1606_07822_b200" / "csrc" / "cg_hogwild.cu").read_bytes()).hexdigest()[:16]
+    sys.path.insert(0, str(ROOT / "tools"))
+    from ncu_summary import kernel_sha16
+
+    src_sha = kernel_sha16()
     traffic = l2_traffic = None
     traffic_current = False
     prof = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
@@ -431,7 +433,8 @@ def main():
                  "peak_tfma_s": fp32_peak / 1e12, "frac": fp32_achieved / fp32_peak,
                  "note": "3 D FMAs per (pair, path step); peak = SMs x 128 FMA/clk x median SM clock"},
         "fp32_frac": fp32_achieved / fp32_peak,
-        "kernel": "hog5_kernel (K1)", "kernel_ms_per_launch": per_launch_ms,
+        "kernel": {5: "hog5_kernel (K1 v5)", 7: "hog7_kernel (K1 v7)", 0: "hog_generic_kernel (K1)"}.get(
+            (agg.get("geometry") or {}).get("kernel"), "K1"), "kernel_ms_per_launch": per_launch_ms,
     }
 
     # end to end through the public API with host buffers (pinned): ids H2D, model init,

@@ -191,7 +191,7 @@ typedef struct cg_epoch_stats {
     int32_t smem_rows;       /* hogwild: of cached_rows, those held in shared memory (the rest: L2 tier) */
     int32_t floor_rows;      /* hogwild: the stability floor of this launch (0 when disabled) */
     int32_t flush_centers;   /* hogwild: merged centers per CTA between flushes (u x worker warps) */
-    int32_t pad;
+    int32_t kernel;          /* hogwild: K1 version run (5, 7; 0 = the generic kernel) */
 } cg_epoch_stats;
 
 /* stream: a cudaStream_t (NULL = legacy default stream). device: CUDA ordinal. */
@@ -233,9 +233,9 @@ CG_API int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floa
  * trained since the last sync (the sync interval). */
 CG_API int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_replica);
 /* The per-row scale of the summed delta for a row on a share q of the updates, n_replicas
- * replicas of `centers` kept centers each per sync: min(1, max(1 / (p n), 32 / (n q centers)))
+ * replicas of `centers` kept centers each per sync: min(1, max(1 / (p n), 128 / (n q centers)))
  * with p = 1 - (1 - q)^centers -- rows few replicas touch are summed as in the reference, a
- * row every replica updates from the same snapshot gets at most 32 stale updates' worth and
+ * row every replica updates from the same snapshot gets at most 128 stale updates' worth and
  * at least the replicas' average. Host-only arithmetic (no device needed). */
 CG_API float cg_sync_row_scale(double q, int32_t n_replicas, double centers);
 

@@ -92,7 +92,7 @@ class CgEpochStats(C.Structure):
         ("smem_rows", C.c_int32),
         ("floor_rows", C.c_int32),
         ("flush_centers", C.c_int32),
-        ("pad", C.c_int32),
+        ("kernel", C.c_int32),
     ]
 
 

@@ -802,16 +802,17 @@ int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* bytes, int
 // `centers` kept centers between syncs. The reference's workers all add
 // into one model (trainer.hpp:72-74, 249-253), so deltas are summed across replicas, but
 // a row every replica updates from the same snapshot receives n x q x centers stale
-// updates per sync: the sum is capped at H = 32 stale updates' worth and never scaled
+// updates per sync: the sum is capped at H = 128 stale updates' worth and never scaled
 // below the average of the replicas that touched it (the per-CTA flush rule of K1, with
-// replicas for CTAs).
+// replicas for CTAs; replicas see their own updates between syncs, and tolerate 4x the
+// staleness of a CTA's write-combined cache rows: profiles/r2_replica*_c1.jsonl).
 float cg_sync_row_scale(double q, int32_t n_replicas, double centers) {
     if (n_replicas <= 1) return 1.0f;
     q = std::min(std::max(q, 0.0), 1.0);
     const double n = static_cast<double>(n_replicas);
     const double p = 1.0 - std::pow(1.0 - q, std::max(centers, 0.0));
     const double avg = 1.0 / std::max(1.0, p * n);
-    static const double H = std::getenv("CG_SYNC_H") ? std::atof(std::getenv("CG_SYNC_H")) : 32.0;
+    constexpr double H = 128.0;  // stable to 256 at N = 8 on C1; 512 diverged (profiles/r2_replica2_*)
     const double stale = H / std::max(1e-30, n * q * centers);
     return static_cast<float>(std::min(1.0, std::max(avg, stale)));
 }
@@ -868,7 +869,7 @@ int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
         if (!t) invalid("null tuning");
         if (t->smem_cache_rows > cgk::kMaxCacheRows) invalid("smem_cache_rows out of range");
-        if (t->kernel != 0 && t->kernel != 5 && t->kernel != 7) invalid("kernel must be 0, 5 or 7");
+        if (t->kernel != 0 && t->kernel != 5 && t->kernel != 7 && t->kernel != 8) invalid("kernel must be 0, 5, 7 or 8");
         s->tune = *t;
     });
 }
@@ -957,9 +958,16 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             const int blocks = s->tune.blocks > 0 ? s->tune.blocks : sms;
             // K1 version: v7 (tensor cores) or v5; the warps in flight set the stability floor
             cgk::HogGeometry g{};
-            bool v7 = s->tune.kernel == 7 &&
-                      cgk::hog7_plan(s->Dp / 4, std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0, blocks,
-                                     s->tune.warps_per_block, s->tune.centers_per_warp, n, s->max_depth, &g);
+            auto plan_tc = [&](int32_t rows, int32_t ctx) {
+                if (s->tune.kernel == 8)
+                    return cgk::hog8_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block, s->tune.centers_per_warp, n,
+                                          s->max_depth, &g);
+                if (s->tune.kernel == 7)
+                    return cgk::hog7_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block, s->tune.centers_per_warp, n,
+                                          s->max_depth, &g);
+                return false;
+            };
+            bool v7 = plan_tc(std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0);
             const double inflight =
                 static_cast<double>(blocks) * (v7 ? g.warps : cgk::hog_max_warps(s->Dp / 4, s->max_depth));
             int32_t floor_rows = 0;
@@ -981,9 +989,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                    s->ctx_share[static_cast<size_t>(ctx_rows)] * inflight >= kHotUpdaters)
                 ++ctx_rows;
             h.dummy_row = s->V - 1;
-            if (v7)
-                v7 = cgk::hog7_plan(s->Dp / 4, want_rows, ctx_rows, blocks, s->tune.warps_per_block,
-                                    s->tune.centers_per_warp, n, s->max_depth, &g);
+            if (v7) v7 = plan_tc(want_rows, ctx_rows);
             if (!v7)
                 g = cgk::hog_plan(h.d4, s->max_depth, want_rows, s->tune.smem_cache_rows, s->tune.blocks,
                                   s->tune.warps_per_block, s->tune.centers_per_warp, s->cfg.window, n, ctx_rows);
@@ -996,7 +1002,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // The L2 tier: rows [S, K) of every CTA's cache, zeroed before each launch (the
             // kernel leaves it zero; re-zeroing keeps an aborted launch from leaking deltas).
             const size_t t2n = static_cast<size_t>(g.blocks) *
-                               static_cast<size_t>(g.cache_rows - g.smem_rows + (g.variant == 7 ? g.ctx_rows : 0)) * s->Dp;
+                               static_cast<size_t>(g.cache_rows - g.smem_rows + (g.variant >= 7 ? g.ctx_rows : 0)) * s->Dp;
             h.tier2 = nullptr;
             if (t2n > 0) {
                 if (s->tier2.n < t2n) s->tier2.alloc(t2n);
@@ -1070,6 +1076,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             out.smem_rows = g.smem_rows;
             out.floor_rows = floor_rows;
             out.flush_centers = h.flush_centers;
+            out.kernel = g.variant >= 7 ? g.variant : (g.variant == 0 ? 0 : 5);
             out.worker_warps = g.warps;
             out.ctx_batch = g.ctx_batch;
             out.blocks = g.blocks;

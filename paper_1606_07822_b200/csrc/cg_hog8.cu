@@ -1,0 +1,454 @@
+// cg_hog8.cu -- K1 v8: Hogwild skip-gram HS training with each center's products on the
+// tensor cores, operands staged as fp16.
+//
+// Same formulation as v7 (cg_hog7.cu): per center and batch of contexts,
+//     S = V U^T,  G = (1 - turn - sigmoid(S)) alpha (masked),  H = G U,  dU = G^T V
+// (trainer.hpp:160-173), with v += h and u += du leaving the accumulator fragments through
+// red.global.add.v2.f32. The rows are converted to fp16 as they are staged (10 mantissa bits,
+// the same operand precision as TF32 but rounded to nearest; the fp32 model in HBM is
+// unchanged), which halves each warp's shared memory -- the limit on warps per SM at
+// D 200/300 in v7 -- and lets every fragment load be one ldmatrix: m8n8.x4 for row-major
+// operands, .trans for the transposed ones (U as H's B, G^T as dU's A, V as dU's B). The
+// products are mma.sync m16n8k16 f16 with fp32 accumulation. Row strides are 8 (mod 16)
+// halves, so the eight 16-byte rows of every ldmatrix land in distinct banks.
+//
+// The per-CTA node cache (NodeCache, trainer.hpp:75-138) is v7's: the K cached syn1 rows and
+// the most frequent words' syn0 rows take their updates in CTA-private delta rows in L2,
+// drained at each flush by atomic exchange and added to the model scaled per row.
+#include <algorithm>
+#include <cstdint>
+
+#include <cuda_fp16.h>
+
+#include "cg_device.cuh"
+#include "cg_kernels.h"
+
+namespace cgk {
+namespace {
+
+using namespace cgdev;
+
+constexpr int kVRows = 16;     // context rows per batch: M of one mma tile
+constexpr int kGhStride = 40;  // fp16 G scratch [16 contexts][32 path rows], 80-byte rows
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const __half* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const __half* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+__device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// red.global.add.v2.f32 under a predicate (no branch around it)
+__device__ __forceinline__ void red_add2_if(bool pred, float* p, float x, float y) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q red.global.add.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
+                 "f"(x), "f"(y), "r"(static_cast<unsigned>(pred))
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t half2_bits(float a, float b) {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// fp16 row stride (halves) for rows of dp floats: dp rounded up to 16 (the mma K step),
+// plus 8 -- 8 (mod 16) halves, an odd number of 16-byte chunks.
+__host__ __device__ constexpr int k8_stride(int dp) { return (dp + 15) / 16 * 16 + 8; }
+// Per-warp bytes: G scratch | V (kVRows rows) | U (urows rows) | codes (32 ints).
+__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int urows) {
+    return static_cast<uint32_t>(kVRows * kGhStride * 2 + (kVRows + urows) * ssh * 2 + 32 * 4);
+}
+
+// S = V U^T for NP pairs of 8-row n-tiles over K16 k-steps of 16 columns. The A fragment of
+// each k-step is one ldmatrix.x4 of V; the B fragments of two n-tiles one ldmatrix.x4 of U.
+template <int NP, int K16>
+__device__ __forceinline__ void s_phase(const __half* V, const __half* U, int ssh, int k16, int lane, float (&acc)[4][4]) {
+    const int m = lane >> 3, rr = lane & 7;
+    const __half* pa = V + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
+    const __half* pb = U + (rr + 8 * (m >> 1)) * ssh + 8 * (m & 1);
+    const int n16 = K16 > 0 ? K16 : k16;
+#pragma unroll 2
+    for (int ks = 0; ks < n16; ++ks) {
+        uint32_t a[4];
+        ldsm_x4(a, pa + 16 * ks);
+#pragma unroll
+        for (int np = 0; np < NP; ++np) {
+            uint32_t b[4];
+            ldsm_x4(b, pb + 16 * np * ssh + 16 * ks);
+            mma_f16(acc[2 * np], a, b[0], b[1]);
+            mma_f16(acc[2 * np + 1], a, b[2], b[3]);
+        }
+    }
+}
+
+// H = G U over KS k-steps of 16 path rows; each pair of 8-column tiles goes to the context
+// rows g, g + 8 (columns below dp only).
+template <int KS, int K16>
+__device__ __forceinline__ void h_phase(const __half* GH, const __half* U, int ssh, int k16, int dp, int lane, float* p0,
+                                        float* p1, bool w0, bool w1) {
+    const int m = lane >> 3, rr = lane & 7, t = lane & 3;
+    uint32_t a[KS][4];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) ldsm_x4(a[kk], GH + (rr + 8 * (m & 1)) * kGhStride + 16 * kk + 8 * (m >> 1));
+    const __half* pb = U + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
+    const int n16 = K16 > 0 ? K16 : k16;
+#pragma unroll 2
+    for (int np = 0; np < n16; ++np) {
+        float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            uint32_t b[4];
+            ldsm_x4_t(b, pb + 16 * kk * ssh + 16 * np);
+            mma_f16(c0, a[kk], b[0], b[1]);
+            mma_f16(c1, a[kk], b[2], b[3]);
+        }
+        const int d0 = 16 * np + 2 * t, d1 = d0 + 8;
+        red_add2_if(w0, p0 + d0, c0[0], c0[1]);
+        red_add2_if(w1, p1 + d0, c0[2], c0[3]);
+        red_add2_if(w0 && d1 < dp, p0 + d1, c1[0], c1[1]);
+        red_add2_if(w1 && d1 < dp, p1 + d1, c1[2], c1[3]);
+    }
+}
+
+// dU = G^T V for MT m-tiles of 16 path rows (one k-step: the batch's 16 contexts).
+template <int MT, int K16>
+__device__ __forceinline__ void u_phase(const __half* GH, const __half* V, int ssh, int k16, int dp, int lane,
+                                        float* const (&pr)[4], const bool (&pw)[4]) {
+    const int m = lane >> 3, rr = lane & 7, t = lane & 3;
+    uint32_t a[MT][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) ldsm_x4_t(a[mt], GH + (rr + 8 * (m >> 1)) * kGhStride + 16 * mt + 8 * (m & 1));
+    const __half* pb = V + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
+    const int n16 = K16 > 0 ? K16 : k16;
+#pragma unroll 2
+    for (int np = 0; np < n16; ++np) {
+        uint32_t b[4];
+        ldsm_x4_t(b, pb + 16 * np);
+        const int d0 = 16 * np + 2 * t, d1 = d0 + 8;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+            mma_f16(c0, a[mt], b[0], b[1]);
+            mma_f16(c1, a[mt], b[2], b[3]);
+            red_add2_if(pw[2 * mt], pr[2 * mt] + d0, c0[0], c0[1]);
+            red_add2_if(pw[2 * mt + 1], pr[2 * mt + 1] + d0, c0[2], c0[3]);
+            red_add2_if(pw[2 * mt] && d1 < dp, pr[2 * mt] + d1, c1[0], c1[1]);
+            red_add2_if(pw[2 * mt + 1] && d1 < dp, pr[2 * mt + 1] + d1, c1[2], c1[3]);
+        }
+    }
+}
+
+// DCH: float4 chunks of a row per lane (staging); WARPS: launch bound; D4 > 0: the row
+// width (Dp / 4) of a benchmark configuration (constant loop bounds and offsets).
+template <int DCH, int WARPS, int D4>
+__global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
+    extern __shared__ __align__(16) unsigned char k8_raw[];
+    constexpr int K16 = D4 > 0 ? (4 * D4 + 15) / 16 : 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int warps = blockDim.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int d4 = D4 > 0 ? D4 : a.d4;
+    const int dp = 4 * d4, k16 = (dp + 15) / 16;
+    const int ssh = D4 > 0 ? k8_stride(4 * D4) : a.smem_stride;
+    const int UR = a.urows;
+    const int K = a.cache_rows, K0 = a.ctx_cache_rows;
+    const int nwords = (K + 31) >> 5;
+    unsigned char* base = k8_raw + ((128u - (smem_u32(k8_raw) & 127u)) & 127u);
+    float* sig = reinterpret_cast<float*>(base);
+    unsigned* touch = reinterpret_cast<unsigned*>(base + 4096);
+    unsigned char* wbase = base + 4096 + ((nwords * 4 + 127) & ~127);
+    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, UR);
+    __half* GH = reinterpret_cast<__half*>(wp);
+    __half* V = GH + kVRows * kGhStride;
+    __half* U = V + kVRows * ssh;
+    int* codes = reinterpret_cast<int*>(U + UR * ssh);
+    float* t2 = a.tier2 ? a.tier2 + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(K + K0) * dp : nullptr;
+    float* t2c = t2 ? t2 + static_cast<size_t>(K) * dp : nullptr;
+    __shared__ int s_done;
+    __shared__ unsigned s_merged;
+
+    for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
+    for (int i = tid; i < nwords; i += blockDim.x) touch[i] = 0u;
+    {  // staging zeroed once: the columns past a row and the padded rows stay finite
+        const int n = static_cast<int>(warps * k8_warp_bytes(ssh, UR) / 16);
+        for (int i = tid; i < n; i += blockDim.x) reinterpret_cast<uint4*>(wbase)[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (tid == 0) {
+        s_done = 0;
+        s_merged = 0;
+    }
+    __syncthreads();
+
+    // ---- the CTA's cache flush: the touched rows' pending deltas (all of them at the end)
+    // are taken with an atomic exchange and added to the model scaled per row.
+    auto drain_row = [&](float* src, float* dst, float sc) {
+#pragma unroll
+        for (int k = 0; k < DCH; ++k) {
+            const int q = lane + 32 * k;
+            if (k < DCH - 1 || q < d4) {
+                const float4 dlt = atom_take4(src + 4 * q);
+                if (nonzero4(dlt)) red_add4(dst + 4 * q, scale4(sc, dlt));
+            }
+        }
+    };
+    auto flush_cache = [&](bool all) {
+        for (int w0 = 0; w0 < nwords; w0 += 32) {
+            const int w = w0 + lane;
+            unsigned m = 0;
+            if (w < nwords) {
+                if (all) {
+                    m = w == nwords - 1 && (K & 31) ? (1u << (K & 31)) - 1u : ~0u;
+                    touch[w] = 0u;
+                } else if (touch[w]) {
+                    m = atomicExch(&touch[w], 0u);
+                }
+            }
+            for (unsigned live = __ballot_sync(kFull, m != 0); live; live &= live - 1) {
+                const int src = __ffs(live) - 1;
+                for (unsigned mm = __shfl_sync(kFull, m, src); mm; mm &= mm - 1) {
+                    const int r = ((w0 + src) << 5) + __ffs(mm) - 1;
+                    drain_row(t2 + static_cast<size_t>(r) * dp, a.syn1 + static_cast<size_t>(r) * dp,
+                              a.row_scale ? a.row_scale[r] : a.hot_flush_scale);
+                }
+            }
+        }
+        for (int r = 0; r < K0; ++r)
+            drain_row(t2c + static_cast<size_t>(r) * dp, a.syn0 + static_cast<size_t>(r) * dp,
+                      a.row_scale ? a.row_scale[K + r] : a.hot_flush_scale);
+        __threadfence();  // the other SMs see this flush before the CTA's next one
+    };
+
+    // rows -> fp16 in shared memory: 16-byte loads through L2 (ld.global.cg: rows other
+    // SMs update with red), packed to half2 pairs (round to nearest), 8-byte stores
+    auto stage_rows = [&](__half* dst0, int nrows, auto&& src_of) {
+        for (int r0 = 0; r0 < nrows; r0 += 4) {
+            float4 v[4][DCH];
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                const float* s = src_of(min(r0 + rr, nrows - 1));
+#pragma unroll
+                for (int k = 0; k < DCH; ++k) {
+                    const int q = lane + 32 * k;
+                    v[rr][k] = (k < DCH - 1 || q < d4) ? ld_cg4(s + 4 * q) : f4(0.f);
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+                if (r0 + rr >= nrows) break;
+                __half* d = dst0 + (r0 + rr) * ssh;
+#pragma unroll
+                for (int k = 0; k < DCH; ++k) {
+                    const int q = lane + 32 * k;
+                    if (k < DCH - 1 || q < d4)
+                        *reinterpret_cast<uint2*>(d + 4 * q) = make_uint2(half2_bits(v[rr][k].x, v[rr][k].y),
+                                                                          half2_bits(v[rr][k].z, v[rr][k].w));
+                }
+            }
+        }
+    };
+
+    const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
+    const int cpw = a.centers_per_warp;
+    unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
+    for (;;) {
+        long long c0 = 0;
+        if (lane == 0) c0 = static_cast<long long>(atomicAdd(a.counters, static_cast<unsigned long long>(cpw)));
+        c0 = __shfl_sync(kFull, c0, 0);
+        if (c0 >= n_kept) break;
+        const int64_t cend = min(static_cast<int64_t>(c0) + cpw, n_kept);
+        int t_p0 = 0, t_len = 0;
+        float t_alpha = 0.f;
+        if (c0 + lane < cend) {
+            const int32_t cj = a.kept[c0 + lane];
+            t_alpha = a.sent_alpha[(c0 + lane) / kSentence];
+            t_p0 = a.path_off[cj];
+            t_len = a.path_off[cj + 1] - t_p0;
+        }
+        for (int64_t ci = c0; ci < cend; ++ci) {
+            const int jt = static_cast<int>(ci - c0);
+            const int64_t s_lo = ci / kSentence * kSentence;
+            const int64_t s_hi = min(s_lo + kSentence, n_kept);
+            const float alpha = __shfl_sync(kFull, t_alpha, jt);
+            const int p0 = __shfl_sync(kFull, t_p0, jt);
+            const int L = __shfl_sync(kFull, t_len, jt);
+            // shrink_window (trainer.hpp:66-68): b = W - draw mod W, the draw reduced by a
+            // 32x32 multiply-high of its top bits (uniform to within W / 2^32)
+            const int b = a.window - static_cast<int>(__umulhi(static_cast<unsigned>(ctr_draw(a.win_key, static_cast<uint64_t>(ci)) >> 32),
+                                                               static_cast<unsigned>(a.window)));
+            const int64_t lo = max(s_lo, ci - b), hi = min(s_hi - 1, ci + b);
+            ++n_centers;
+            const int n = static_cast<int>(hi - lo);
+            if (n == 0) continue;
+            bool touched_cache = false;
+            for (int q0 = 0; q0 < n; q0 += kVRows) {
+                const int nb = min(kVRows, n - q0);
+                int xid = 0;
+                if (lane < nb) {
+                    int64_t pos = lo + q0 + lane;
+                    pos += pos >= ci;  // skip the center's own position
+                    xid = a.kept[pos];
+                }
+                const unsigned hot_ctx = __ballot_sync(kFull, lane < nb && xid < K0);
+                const int x0 = __shfl_sync(kFull, xid, g), x1 = __shfl_sync(kFull, xid, (g + 8) & 31);
+                float* pc0 = ((hot_ctx >> g) & 1u ? t2c : a.syn0) + static_cast<size_t>(x0) * dp;
+                float* pc1 = ((hot_ctx >> (g + 8)) & 1u ? t2c : a.syn0) + static_cast<size_t>(x1) * dp;
+                const bool w0 = g < nb, w1 = g + 8 < nb;
+                for (int jc = 0; jc < L; jc += UR) {
+                    const int Lc = min(UR, L - jc);
+                    const bool restage = q0 == 0 || L > UR;  // U is kept across the batches of one chunk
+                    int code = 0;
+                    if (lane < Lc) code = a.path_code[p0 + jc + lane];
+                    const int row = code >> 1;
+                    __syncwarp();  // the previous chunk / batch is done with V, U and G
+                    // the batch's context rows (first chunk) and the chunk's path rows, as fp16
+                    if (jc == 0)
+                        stage_rows(V, nb, [&](int i) { return a.syn0 + static_cast<size_t>(__shfl_sync(kFull, xid, i)) * dp; });
+                    if (restage) {
+                        stage_rows(U, Lc, [&](int j) { return a.syn1 + static_cast<size_t>(__shfl_sync(kFull, row, j)) * dp; });
+                        codes[lane] = code;
+                    }
+                    __syncwarp();
+                    // ---- S = V U^T, then G (masked, fp16) into the G scratch ----
+                    const int NP = (Lc + 15) >> 4;  // pairs of 8-row n-tiles (16 path rows)
+                    float acc[4][4];
+#pragma unroll
+                    for (int n2 = 0; n2 < 4; ++n2) acc[n2][0] = acc[n2][1] = acc[n2][2] = acc[n2][3] = 0.f;
+                    if (NP == 1) s_phase<1, K16>(V, U, ssh, k16, lane, acc);
+                    else s_phase<2, K16>(V, U, ssh, k16, lane, acc);
+#pragma unroll
+                    for (int n2 = 0; n2 < 4; ++n2) {
+                        if (n2 >= 2 * NP) break;
+                        float gv[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = g + (e >> 1) * 8, j = 8 * n2 + 2 * t + (e & 1);
+                            gv[e] = 0.f;
+                            if (i < nb && j < Lc)
+                                gv[e] = (1.0f - static_cast<float>(codes[j] & 1) - table_sigmoid(sig, acc[n2][e], a.sig_scale)) * alpha;
+                        }
+                        *reinterpret_cast<uint32_t*>(GH + g * kGhStride + 8 * n2 + 2 * t) = half2_bits(gv[0], gv[1]);
+                        *reinterpret_cast<uint32_t*>(GH + (g + 8) * kGhStride + 8 * n2 + 2 * t) = half2_bits(gv[2], gv[3]);
+                    }
+                    __syncwarp();
+                    // ---- H = G U -> the context rows (v += h, trainer.hpp:173) ----
+                    if (NP == 1) h_phase<1, K16>(GH, U, ssh, k16, dp, lane, pc0, pc1, w0, w1);
+                    else h_phase<2, K16>(GH, U, ssh, k16, dp, lane, pc0, pc1, w0, w1);
+                    // ---- dU = G^T V -> the path rows (syn1, or the CTA's delta of a cached row) ----
+                    float* pr[4];
+                    bool pw[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int j = g + 8 * e;  // m-tile e / 2, rows g and g + 8
+                        const int rj = __shfl_sync(kFull, row, j);
+                        pw[e] = j < Lc;
+                        pr[e] = (rj < K ? t2 : a.syn1) + static_cast<size_t>(rj) * dp;
+                    }
+                    if (NP == 1) u_phase<1, K16>(GH, V, ssh, k16, dp, lane, pr, pw);
+                    else u_phase<2, K16>(GH, V, ssh, k16, dp, lane, pr, pw);
+                    const bool cached = lane < Lc && row < K;
+                    if (__any_sync(kFull, cached)) {
+                        touched_cache = true;
+                        if (cached) {
+                            const unsigned bit = 1u << (row & 31);
+                            if (!(touch[row >> 5] & bit)) atomicOr(&touch[row >> 5], bit);
+                        }
+                    }
+                }
+                if (hot_ctx) touched_cache = true;
+            }
+            n_pairs += static_cast<unsigned long long>(n);
+            n_steps += static_cast<unsigned long long>(n) * static_cast<unsigned long long>(L);
+            if (touched_cache) {
+                unsigned m = 0;
+                if (lane == 0) m = atomicAdd(&s_merged, 1u) + 1u;
+                m = __shfl_sync(kFull, m, 0);
+                if (m % static_cast<unsigned>(a.flush_centers) == 0u) flush_cache(false);
+            }
+        }
+    }
+    int last = 0;
+    if (lane == 0) {
+        atomicAdd(a.counters + 1, n_pairs);
+        atomicAdd(a.counters + 2, n_steps);
+        atomicAdd(a.counters + 3, n_centers);
+        __threadfence_block();
+        last = atomicAdd(&s_done, 1) == warps - 1;
+    }
+    last = __shfl_sync(kFull, last, 0);
+    if (last && (K > 0 || K0 > 0)) flush_cache(true);
+}
+
+constexpr int kV8MaxWarps = 16;
+
+template <int DCH, int D4>
+void launch8(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
+    auto k = hog8_kernel<DCH, kV8MaxWarps, D4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
+    k<<<g.blocks, g.warps * 32, g.smem, s>>>(a);
+}
+
+}  // namespace
+
+bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
+               int max_depth, HogGeometry* g) {
+    if (d4 > 96) return false;
+    const int dp = 4 * d4;
+    const int ssh = k8_stride(dp);
+    const int nwords = (cache_rows + 31) / 32;
+    const size_t fixed = 4096 + ((static_cast<size_t>(nwords) * 4 + 127) & ~size_t{127}) + 128;
+    const size_t budget = 227 * 1024 - 1024;
+    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, ur)); };
+    // Path rows staged per chunk: the deepest path when it fits in 32 rows, 16 where 32
+    // would leave fewer than 10 warps; a deeper path trains in chunks (contexts stay staged).
+    int urows = max_depth > 16 ? 32 : 16;
+    if (urows == 32 && warps_for(32) < 10) urows = 16;
+    int warps = std::min(kV8MaxWarps, warps_for(urows));
+    if (warps_override > 0) warps = std::min(warps, warps_override);
+    if (warps < 1) return false;
+    g->variant = 8;
+    g->warps = warps;
+    g->blocks = blocks;
+    g->cache_rows = cache_rows;
+    g->smem_rows = 0;
+    g->ctx_rows = ctx_rows;
+    g->ctx_batch = kVRows;
+    g->flusher = false;
+    g->urows = urows;
+    g->smem_stride = ssh;
+    g->specialise = true;
+    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, urows);
+    g->cpw = cpw_override > 0 ? std::min(cpw_override, 32)
+                              : (tokens / (static_cast<int64_t>(blocks) * warps) >= 2000 ? 16 : 8);
+    return true;
+}
+
+void launch_hog8(const HogArgs& a0, const HogGeometry& g, cudaStream_t s) {
+    HogArgs a = a0;
+    a.cache_rows = g.cache_rows;
+    a.smem_rows = 0;
+    a.ctx_cache_rows = g.ctx_rows;
+    a.centers_per_warp = g.cpw;
+    a.ctx_batch = kVRows;
+    a.flusher = 0;
+    a.urows = g.urows;
+    a.smem_stride = g.smem_stride;
+    const int dch = (a.d4 + 31) / 32;
+    switch (a.d4) {  // the benchmark row widths (D 100, 128, 200, 300 padded to 8 floats)
+        case 26: launch8<1, 26>(a, g, s); return;
+        case 32: launch8<1, 32>(a, g, s); return;
+        case 50: launch8<2, 50>(a, g, s); return;
+        case 76: launch8<3, 76>(a, g, s); return;
+        default: break;
+    }
+    if (dch == 1) launch8<1, 0>(a, g, s);
+    else if (dch == 2) launch8<2, 0>(a, g, s);
+    else launch8<3, 0>(a, g, s);
+}
+
+}  // namespace cgk

@@ -31,7 +31,7 @@
 #define CG_W2 12  // warps per CTA the D <= 256 variant is compiled for (experiments: tools/ab_build.py)
 #endif
 #ifndef CG_T2_READ
-#define CG_T2_READ 1  // 1: warps read an L2-tier cached row as base + their CTA's pending delta; 0: base only
+#define CG_T2_READ 0  // 0: warps read the L2-tier cached rows flushed state (write-combining); 1: + their CTA pending delta
 #endif
 #ifndef CG_STAGE_BULK
 #define CG_STAGE_BULK 1  // 1: rows staged by bulk copies (TMA unit, UBLKCP); 0: cp.async (LDGSTS)
@@ -1038,6 +1038,7 @@ HogGeometry hog_plan(int d4, int max_depth, int cache_rows, int smem_rows, int b
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     switch (g.variant) {
         case 7: launch_hog7(a, g, s); break;
+        case 8: launch_hog8(a, g, s); break;
         case 0: {
             auto k = hog_generic_kernel<kGenericWarps>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));

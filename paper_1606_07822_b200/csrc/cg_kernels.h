@@ -142,7 +142,7 @@ struct HogGeometry {
     int cache_rows;   // K (both tiers)
     int smem_rows;    // S
     int ctx_batch;    // contexts staged per warp
-    int variant;      // 7 = the tensor-core kernel; 1..3 = v5 (float4 chunks per lane); 0 = generic
+    int variant;      // 8 / 7 = the tensor-core kernels; 1..3 = v5 (float4 chunks per lane); 0 = generic
     bool specialise;  // use the row-width-specialised instantiation when there is one
     bool flusher;     // one extra (flusher) warp; only when registers leave room for it
     int ctx_rows;     // cached syn0 rows (most frequent context words)
@@ -169,6 +169,10 @@ void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 bool hog7_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
                int max_depth, HogGeometry* g);
 void launch_hog7(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
+// K1 v8 (cg_hog8.cu): v7 with fp16-staged operands, ldmatrix fragments and m16n8k16 f16 mma.
+bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
+               int max_depth, HogGeometry* g);
+void launch_hog8(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 // ---------------- evaluation (cg_eval.cu) -----------------------------------------
 // Row stride of a normalised table: dim rounded up to the scoring kernels' k-chunk.

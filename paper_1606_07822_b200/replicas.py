@@ -8,7 +8,7 @@ semantics: every ``sync_words`` words per replica each replica's delta since the
 sync (model - snapshot) is all-reduced with SUM (NCCL over NVLink/NVSwitch at N > 1;
 gloo on CPU in the tests) and applied to the snapshot row by row with the sync scale
 (cg_session_sync_apply / cg_sync_row_scale: rows few replicas touched are summed, a row
-every replica updated from the same snapshot gets at most 32 stale updates' worth and at
+every replica updated from the same snapshot gets at most 128 stale updates' worth and at
 least the replicas' average). The learning rate follows the global schedule estimated as
 N x local progress. ``mode="average"`` keeps round 1's whole-model averaging (local SGD
 with model averaging) for comparison.

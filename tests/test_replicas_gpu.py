@@ -17,7 +17,9 @@ from paper_1606_07822_b200 import _lib, api
 pytestmark = pytest.mark.gpu
 
 # delta-sync interval per replica for the split-corpus tests (tools/replica_quality.py)
-SYNC_WORDS = {"c1": 50_000, "c2": 250_000}
+# (C1 is a 1M-token corpus: a replica's hot rows see 1/N of its updates between syncs, so it
+# needs short periods; C2 learns like one replica at any period measured, 100k-1M)
+SYNC_WORDS = {"c1": 500, "c2": 250_000}
 
 
 def test_average_buffers_exact():

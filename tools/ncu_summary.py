@@ -30,6 +30,19 @@ def raw(rep):
     return r[0], r[1], r[2:]
 
 
+def kernel_sha16() -> str:
+    """Hash of the K1 sources (bench.py compares it to decide whether a capture is current)."""
+    import hashlib
+    from pathlib import Path
+
+    csrc = Path(__file__).resolve().parents[1] / "paper_1606_07822_b200" / "csrc"
+    h = hashlib.sha256()
+    for name in ("cg_hogwild.cu", "cg_hog7.cu", "cg_device.cuh"):
+        if (csrc / name).exists():
+            h.update((csrc / name).read_bytes())
+    return h.hexdigest()[:16]
+
+
 def to_bytes(v, unit):
     return float(v.replace(",", "")) * SCALE.get(unit, 1)
 
@@ -69,9 +82,13 @@ def main():
             print(f"L2 traffic per launch: {l2:.4g} bytes (lts__t_sectors x 32 B) = {l2 / t_s / 1e9:.0f} GB/s")
         print()
         if a.traffic_json:
+            t_i = h.index("gpu__time_duration.sum")
             with open(a.traffic_json, "w") as f:
                 json.dump({"kernel": row[name_i][:100], "dram_bytes_per_launch": rd + wr, "dram_read": rd,
-                           "dram_write": wr, "l2_bytes_per_launch": l2, "report": a.rep}, f, indent=1)
+                           "dram_write": wr, "l2_bytes_per_launch": l2, "report": a.rep,
+                           "ncu_kernel_time": f"{row[t_i]} {units[t_i]}",
+                           # the K1 sources this capture was taken of (bench.py flags stale captures)
+                           "kernel_sha16": kernel_sha16()}, f, indent=1)
     if a.launches:
         rows = list(csv.reader(open(a.launches)))
         hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
