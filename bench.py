@@ -433,7 +433,7 @@ def main():
                  "peak_tfma_s": fp32_peak / 1e12, "frac": fp32_achieved / fp32_peak,
                  "note": "3 D FMAs per (pair, path step); peak = SMs x 128 FMA/clk x median SM clock"},
         "fp32_frac": fp32_achieved / fp32_peak,
-        "kernel": {5: "hog5_kernel (K1 v5)", 7: "hog7_kernel (K1 v7)", 0: "hog_generic_kernel (K1)"}.get(
+        "kernel": {8: "hog8_kernel (K1 v8)", 5: "hog5_kernel (K1 v5)", 0: "hog_generic_kernel (K1)"}.get(
             (agg.get("geometry") or {}).get("kernel"), "K1"), "kernel_ms_per_launch": per_launch_ms,
     }
 

@@ -191,7 +191,7 @@ typedef struct cg_epoch_stats {
     int32_t smem_rows;       /* hogwild: of cached_rows, those held in shared memory (the rest: L2 tier) */
     int32_t floor_rows;      /* hogwild: the stability floor of this launch (0 when disabled) */
     int32_t flush_centers;   /* hogwild: merged centers per CTA between flushes (u x worker warps) */
-    int32_t kernel;          /* hogwild: K1 version run (5, 7; 0 = the generic kernel) */
+    int32_t kernel;          /* hogwild: K1 version run (8, 5; 0 = the generic kernel) */
 } cg_epoch_stats;
 
 /* stream: a cudaStream_t (NULL = legacy default stream). device: CUDA ordinal. */
@@ -254,8 +254,10 @@ typedef struct cg_tuning {
                                  K is smaller; > 0 = at least this many rows; < 0 = none, K is honoured
                                  literally (K = 0 then diverges on small vocabularies at full-GPU
                                  concurrency) */
-    int32_t kernel;           /* 0 = default; 5 = v5 (packed FP32 FMA, two-tier cache); 7 = v7 (each center's
-                                 products on the tensor cores, mma.sync TF32) */
+    int32_t kernel;           /* 0 = default: v8, each center's products on the tensor cores (mma.sync f16
+                                 operands, fp32 accumulation), for D <= 384; 5 = v5, FP32 FMA arithmetic
+                                 (packed FFMA2) with a shared-memory tier for the hottest cached rows.
+                                 Rows wider than 384 floats train on the generic FP32 kernel. */
 } cg_tuning;
 CG_API int cg_session_tune(cg_session* s, const cg_tuning* t);
 

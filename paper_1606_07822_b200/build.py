@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libcachegram_b200.so"
-SOURCES = ["cg_capi.cu", "cg_det.cu", "cg_hogwild.cu", "cg_hog7.cu", "cg_hog8.cu", "cg_eval.cu", "cg_ingest.cu", "cg_modelio.cpp"]
+SOURCES = ["cg_capi.cu", "cg_det.cu", "cg_hogwild.cu", "cg_hog8.cu", "cg_eval.cu", "cg_ingest.cu", "cg_modelio.cpp"]
 HEADERS = ["cg_device.cuh", "cg_kernels.h", "cg_host.h"]
 
 NVCC_FLAGS = [

@@ -869,7 +869,7 @@ int cg_session_tune(cg_session* s, const cg_tuning* t) {
     return guarded([&] {
         if (!t) invalid("null tuning");
         if (t->smem_cache_rows > cgk::kMaxCacheRows) invalid("smem_cache_rows out of range");
-        if (t->kernel != 0 && t->kernel != 5 && t->kernel != 7 && t->kernel != 8) invalid("kernel must be 0, 5, 7 or 8");
+        if (t->kernel != 0 && t->kernel != 5 && t->kernel != 8) invalid("kernel must be 0, 5 or 8");
         s->tune = *t;
     });
 }
@@ -956,20 +956,16 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
             const int blocks = s->tune.blocks > 0 ? s->tune.blocks : sms;
-            // K1 version: v7 (tensor cores) or v5; the warps in flight set the stability floor
+            // K1 version: v8 (tensor cores) or v5; the warps in flight set the stability floor
             cgk::HogGeometry g{};
+            // v8 (tensor cores) unless the caller asked for v5 (FP32 FMA) or the rows are too wide
             auto plan_tc = [&](int32_t rows, int32_t ctx) {
-                if (s->tune.kernel == 8)
-                    return cgk::hog8_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block, s->tune.centers_per_warp, n,
-                                          s->max_depth, &g);
-                if (s->tune.kernel == 7)
-                    return cgk::hog7_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block, s->tune.centers_per_warp, n,
-                                          s->max_depth, &g);
-                return false;
+                return s->tune.kernel != 5 && cgk::hog8_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block,
+                                                             s->tune.centers_per_warp, n, s->max_depth, &g);
             };
-            bool v7 = plan_tc(std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0);
+            bool v8 = plan_tc(std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0);
             const double inflight =
-                static_cast<double>(blocks) * (v7 ? g.warps : cgk::hog_max_warps(s->Dp / 4, s->max_depth));
+                static_cast<double>(blocks) * (v8 ? g.warps : cgk::hog_max_warps(s->Dp / 4, s->max_depth));
             int32_t floor_rows = 0;
             if (s->tune.min_cache_rows == 0) {
                 for (int32_t r = 0; r < static_cast<int32_t>(s->row_share.size()); ++r)
@@ -989,8 +985,8 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
                    s->ctx_share[static_cast<size_t>(ctx_rows)] * inflight >= kHotUpdaters)
                 ++ctx_rows;
             h.dummy_row = s->V - 1;
-            if (v7) v7 = plan_tc(want_rows, ctx_rows);
-            if (!v7)
+            if (v8) v8 = plan_tc(want_rows, ctx_rows);
+            if (!v8)
                 g = cgk::hog_plan(h.d4, s->max_depth, want_rows, s->tune.smem_cache_rows, s->tune.blocks,
                                   s->tune.warps_per_block, s->tune.centers_per_warp, s->cfg.window, n, ctx_rows);
             if (g.smem == 0) invalid("dim too large for the generic kernel's shared-memory row buffers");
@@ -1076,7 +1072,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             out.smem_rows = g.smem_rows;
             out.floor_rows = floor_rows;
             out.flush_centers = h.flush_centers;
-            out.kernel = g.variant >= 7 ? g.variant : (g.variant == 0 ? 0 : 5);
+            out.kernel = g.variant == 8 ? 8 : (g.variant == 0 ? 0 : 5);
             out.worker_warps = g.warps;
             out.ctx_batch = g.ctx_batch;
             out.blocks = g.blocks;

@@ -1,20 +1,39 @@
-// cg_hog8.cu -- K1 v8: Hogwild skip-gram HS training with each center's products on the
-// tensor cores, operands staged as fp16.
+// cg_hog8.cu -- K1 v8 (the default): Hogwild skip-gram HS training with each center's
+// products on the tensor cores.
 //
-// Same formulation as v7 (cg_hog7.cu): per center and batch of contexts,
-//     S = V U^T,  G = (1 - turn - sigmoid(S)) alpha (masked),  H = G U,  dU = G^T V
-// (trainer.hpp:160-173), with v += h and u += du leaving the accumulator fragments through
-// red.global.add.v2.f32. The rows are converted to fp16 as they are staged (10 mantissa bits,
-// the same operand precision as TF32 but rounded to nearest; the fp32 model in HBM is
-// unchanged), which halves each warp's shared memory -- the limit on warps per SM at
-// D 200/300 in v7 -- and lets every fragment load be one ldmatrix: m8n8.x4 for row-major
-// operands, .trans for the transposed ones (U as H's B, G^T as dU's A, V as dU's B). The
-// products are mma.sync m16n8k16 f16 with fp32 accumulation. Row strides are 8 (mod 16)
-// halves, so the eight 16-byte rows of every ldmatrix land in distinct banks.
+// For one center c with its batch of contexts x_0..x_{n-1} (syn0 rows v_i) and its root-first
+// path rows u_0..u_{L-1} (syn1), train_center (trainer.hpp:147-175) in K1's center-batched
+// order (every context's dots against the rows as loaded: within-center staleness of at most
+// 2W updates, as in v5) is three small matrix products:
+//     S  = V U^T            (n x L)  the dot products            (vec_ops.hpp:14-18)
+//     G  = (1 - turn - sigmoid(S)) * alpha, zero outside the real pairs (trainer.hpp:166-167)
+//     H  = G U              (n x D)  h_i = sum_j g_ij u_j         (trainer.hpp:168)
+//     dU = G^T V            (L x D)  u_j += sum_i g_ij v_i        (trainer.hpp:171)
+// then v_i += h_i (trainer.hpp:173). One warp computes them with mma.sync m16n8k16 (f16
+// operands, fp32 accumulation) out of shared memory: contexts are the M dimension of S and H
+// (16 per tile), path rows the N dimension of S, the K dimension of H and the M dimension of
+// dU. A center costs ~10x fewer instructions than the FP32 FMA kernel (v5), which spends
+// them on per-lane FMAs and the transpose-reduce of the dots.
 //
-// The per-CTA node cache (NodeCache, trainer.hpp:75-138) is v7's: the K cached syn1 rows and
-// the most frequent words' syn0 rows take their updates in CTA-private delta rows in L2,
-// drained at each flush by atomic exchange and added to the model scaled per row.
+// Operands: the rows are converted to fp16 as they are staged -- 10 mantissa bits, rounded
+// to nearest (TF32's operand precision); the fp32 model in HBM is unchanged and every sum
+// is fp32; the sigmoid is the reference's 1000-bucket table (bucket width 0.012), far
+// coarser than the operand rounding. fp16 staging halves a warp's shared memory against
+// fp32 (12 warps per SM at D 200, 8 at D 300, where fp32-staged TF32 operands left 6 and 5:
+// v7, measured slower than v5 for that reason and removed). Staging is pipelined: cp.async
+// lands each row in a slot of the warp's fp32 ring (4 rows in flight, one commit group per
+// row) and each lane converts the chunks it copied. Every fragment load is one ldmatrix --
+// m8n8.x4 for the row-major operands, .trans for U as H's B, G^T as dU's A and V as dU's B;
+// row strides of 8 (mod 16) halves put the eight 16-byte rows of each matrix in distinct
+// banks.
+//
+// H and dU leave straight from the accumulator fragments with red.global.add.v2.f32 (no lost
+// updates, predicated instead of branched). The per-CTA node cache (NodeCache,
+// trainer.hpp:75-138): the K cached syn1 rows and the most frequent words' syn0 rows take
+// their updates in CTA-private delta rows in L2 (`tier2`), which the flush drains by atomic
+// exchange and adds to the model scaled per row; warps read a cached row's flushed state
+// (write-combining: a CTA's own pending delta joins the row at its flush, like every other
+// CTA's).
 #include <algorithm>
 #include <cstdint>
 
@@ -60,9 +79,11 @@ __device__ __forceinline__ uint32_t half2_bits(float a, float b) {
 // fp16 row stride (halves) for rows of dp floats: dp rounded up to 16 (the mma K step),
 // plus 8 -- 8 (mod 16) halves, an odd number of 16-byte chunks.
 __host__ __device__ constexpr int k8_stride(int dp) { return (dp + 15) / 16 * 16 + 8; }
-// Per-warp bytes: G scratch | V (kVRows rows) | U (urows rows) | codes (32 ints).
-__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int urows) {
-    return static_cast<uint32_t>(kVRows * kGhStride * 2 + (kVRows + urows) * ssh * 2 + 32 * 4);
+constexpr int kRing = 4;  // fp32 rows in flight per warp while staging
+// Per-warp bytes: G scratch | V (kVRows rows) | U (urows rows) | codes (32 ints) | fp32 ring
+// (kRing rows of dp floats: cp.async lands rows there, lanes convert them to fp16).
+__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int urows, int dp) {
+    return static_cast<uint32_t>(kVRows * kGhStride * 2 + (kVRows + urows) * ssh * 2 + 32 * 4 + kRing * dp * 4);
 }
 
 // S = V U^T for NP pairs of 8-row n-tiles over K16 k-steps of 16 columns. The A fragment of
@@ -163,11 +184,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     float* sig = reinterpret_cast<float*>(base);
     unsigned* touch = reinterpret_cast<unsigned*>(base + 4096);
     unsigned char* wbase = base + 4096 + ((nwords * 4 + 127) & ~127);
-    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, UR);
+    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, UR, dp);
     __half* GH = reinterpret_cast<__half*>(wp);
     __half* V = GH + kVRows * kGhStride;
     __half* U = V + kVRows * ssh;
     int* codes = reinterpret_cast<int*>(U + UR * ssh);
+    float* ring = reinterpret_cast<float*>(codes + 32);
     float* t2 = a.tier2 ? a.tier2 + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(K + K0) * dp : nullptr;
     float* t2c = t2 ? t2 + static_cast<size_t>(K) * dp : nullptr;
     __shared__ int s_done;
@@ -176,7 +198,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < nwords; i += blockDim.x) touch[i] = 0u;
     {  // staging zeroed once: the columns past a row and the padded rows stay finite
-        const int n = static_cast<int>(warps * k8_warp_bytes(ssh, UR) / 16);
+        const int n = static_cast<int>(warps * k8_warp_bytes(ssh, UR, dp) / 16);
         for (int i = tid; i < n; i += blockDim.x) reinterpret_cast<uint4*>(wbase)[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (tid == 0) {
@@ -224,32 +246,38 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
         __threadfence();  // the other SMs see this flush before the CTA's next one
     };
 
-    // rows -> fp16 in shared memory: 16-byte loads through L2 (ld.global.cg: rows other
-    // SMs update with red), packed to half2 pairs (round to nearest), 8-byte stores
-    auto stage_rows = [&](__half* dst0, int nrows, auto&& src_of) {
-        for (int r0 = 0; r0 < nrows; r0 += 4) {
-            float4 v[4][DCH];
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                const float* s = src_of(min(r0 + rr, nrows - 1));
-#pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    const int q = lane + 32 * k;
-                    v[rr][k] = (k < DCH - 1 || q < d4) ? ld_cg4(s + 4 * q) : f4(0.f);
-                }
-            }
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-                if (r0 + rr >= nrows) break;
-                __half* d = dst0 + (r0 + rr) * ssh;
+    // rows -> fp16 in shared memory, pipelined: cp.async (LDGSTS, through L2 like the rows'
+    // red.global updates) lands each row in a slot of the warp's fp32 ring, one commit group
+    // per row, kRing rows in flight; a lane converts exactly the 16-byte chunks it copied
+    // (so no warp barrier is needed) to half2 pairs (round to nearest) as each row lands.
+    auto stage_rows = [&](int nrows, auto&& src_of, auto&& dst_of) {
+        auto issue = [&](int r) {
+            if (r < nrows) {
+                const float* src = src_of(r);
+                float* slot = ring + (r % kRing) * dp;
 #pragma unroll
                 for (int k = 0; k < DCH; ++k) {
                     const int q = lane + 32 * k;
-                    if (k < DCH - 1 || q < d4)
-                        *reinterpret_cast<uint2*>(d + 4 * q) = make_uint2(half2_bits(v[rr][k].x, v[rr][k].y),
-                                                                          half2_bits(v[rr][k].z, v[rr][k].w));
+                    if (k < DCH - 1 || q < d4) cp_async16(slot + 4 * q, src + 4 * q);
                 }
             }
+            asm volatile("cp.async.commit_group;" ::: "memory");  // empty past the last row
+        };
+#pragma unroll
+        for (int r = 0; r < kRing; ++r) issue(r);
+        for (int r = 0; r < nrows; ++r) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
+            const float* slot = ring + (r % kRing) * dp;
+            __half* d = dst_of(r);
+#pragma unroll
+            for (int k = 0; k < DCH; ++k) {
+                const int q = lane + 32 * k;
+                if (k < DCH - 1 || q < d4) {
+                    const float4 v = *reinterpret_cast<const float4*>(slot + 4 * q);
+                    *reinterpret_cast<uint2*>(d + 4 * q) = make_uint2(half2_bits(v.x, v.y), half2_bits(v.z, v.w));
+                }
+            }
+            issue(r + kRing);
         }
     };
 
@@ -307,11 +335,16 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                     const int row = code >> 1;
                     __syncwarp();  // the previous chunk / batch is done with V, U and G
                     // the batch's context rows (first chunk) and the chunk's path rows, as fp16
-                    if (jc == 0)
-                        stage_rows(V, nb, [&](int i) { return a.syn0 + static_cast<size_t>(__shfl_sync(kFull, xid, i)) * dp; });
-                    if (restage) {
-                        stage_rows(U, Lc, [&](int j) { return a.syn1 + static_cast<size_t>(__shfl_sync(kFull, row, j)) * dp; });
-                        codes[lane] = code;
+                    {  // one pipeline: rows [0, nv) are context rows, then the chunk's path rows
+                        const int nv = jc == 0 ? nb : 0, nu = restage ? Lc : 0;
+                        stage_rows(
+                            nv + nu,
+                            [&](int r) {
+                                return r < nv ? a.syn0 + static_cast<size_t>(__shfl_sync(kFull, xid, r)) * dp
+                                              : a.syn1 + static_cast<size_t>(__shfl_sync(kFull, row, r - nv)) * dp;
+                            },
+                            [&](int r) { return r < nv ? V + r * ssh : U + (r - nv) * ssh; });
+                        if (restage) codes[lane] = code;
                     }
                     __syncwarp();
                     // ---- S = V U^T, then G (masked, fp16) into the G scratch ----
@@ -403,7 +436,7 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     const int nwords = (cache_rows + 31) / 32;
     const size_t fixed = 4096 + ((static_cast<size_t>(nwords) * 4 + 127) & ~size_t{127}) + 128;
     const size_t budget = 227 * 1024 - 1024;
-    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, ur)); };
+    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, ur, dp)); };
     // Path rows staged per chunk: the deepest path when it fits in 32 rows, 16 where 32
     // would leave fewer than 10 warps; a deeper path trains in chunks (contexts stay staged).
     int urows = max_depth > 16 ? 32 : 16;
@@ -422,7 +455,7 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     g->urows = urows;
     g->smem_stride = ssh;
     g->specialise = true;
-    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, urows);
+    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, urows, dp);
     g->cpw = cpw_override > 0 ? std::min(cpw_override, 32)
                               : (tokens / (static_cast<int64_t>(blocks) * warps) >= 2000 ? 16 : 8);
     return true;

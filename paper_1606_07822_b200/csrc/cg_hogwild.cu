@@ -1037,7 +1037,6 @@ HogGeometry hog_plan(int d4, int max_depth, int cache_rows, int smem_rows, int b
 
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
     switch (g.variant) {
-        case 7: launch_hog7(a, g, s); break;
         case 8: launch_hog8(a, g, s); break;
         case 0: {
             auto k = hog_generic_kernel<kGenericWarps>;

@@ -131,8 +131,8 @@ struct HogArgs {
     int32_t dummy_row;         // the all-zero syn1 pad row
     int32_t ctx_batch;         // context rows staged per warp (<= 2 * window)
     int32_t flusher;           // 1 = the block's last warp is a cache flusher (set by the launcher)
-    int32_t urows;             // v7: path rows staged per chunk
-    int32_t smem_stride;       // v7: shared-memory row stride (floats)
+    int32_t urows;             // v8: path rows staged per chunk
+    int32_t smem_stride;       // v8: shared-memory row stride (halves)
     unsigned long long* counters;  // [0] tile ticket, [1] pairs, [2] steps, [3] centers
 };
 struct HogGeometry {
@@ -142,12 +142,12 @@ struct HogGeometry {
     int cache_rows;   // K (both tiers)
     int smem_rows;    // S
     int ctx_batch;    // contexts staged per warp
-    int variant;      // 8 / 7 = the tensor-core kernels; 1..3 = v5 (float4 chunks per lane); 0 = generic
+    int variant;      // 8 = v8 (tensor cores); 1..3 = v5 (FP32, float4 chunks per lane); 0 = generic
     bool specialise;  // use the row-width-specialised instantiation when there is one
     bool flusher;     // one extra (flusher) warp; only when registers leave room for it
     int ctx_rows;     // cached syn0 rows (most frequent context words)
-    int urows;        // v7: path rows staged per chunk
-    int smem_stride;  // v7: shared-memory row stride (floats)
+    int urows;        // v8: path rows staged per chunk
+    int smem_stride;  // v8: shared-memory row stride (halves)
     size_t smem;
 };
 // Most frequent words whose syn0 rows K1 caches per CTA (averaged at flush, like the hot
@@ -164,12 +164,9 @@ int hog_max_warps(int d4, int max_depth);
 HogGeometry hog_plan(int d4, int max_depth, int cache_rows, int smem_rows, int blocks_override, int warps_override,
                      int cpw_override, int window, int64_t tokens, int ctx_rows);
 void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
-// K1 v7 (cg_hog7.cu): each center's products on the tensor cores (mma.sync TF32). Returns
-// false where it does not apply (rows wider than 384 floats, or no warp fits).
-bool hog7_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
-               int max_depth, HogGeometry* g);
-void launch_hog7(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
-// K1 v8 (cg_hog8.cu): v7 with fp16-staged operands, ldmatrix fragments and m16n8k16 f16 mma.
+// K1 v8 (cg_hog8.cu), the default: each center's products on the tensor cores (mma.sync
+// m16n8k16 f16, fp32 accumulation) from fp16-staged rows. Returns false where it does not
+// apply (rows wider than 384 floats, or no warp fits).
 bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
                int max_depth, HogGeometry* g);
 void launch_hog8(const HogArgs& a, const HogGeometry& g, cudaStream_t s);

@@ -50,11 +50,8 @@ GRIDS = {
     "stab": [(31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 32), (31, -1, 0, 10, 3, 256, 16),
              (31, -1, 0, 10, 3, 256, 16), (31, -1, 0, 10, 3, 256, 8), (31, -1, 0, 10, 3, 256, 1),
              (31, -1, 0, 10, 3, 256, 16, 1), (31, -1, 0, 10, 3, 256, 1, 1), (256, -1, 0, 10, 3, 256, 16)],
-    "v7": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (31, -1, 0, 10, 3, 256, 32, 0, 7), (8, -1, -1, 10, 3, 256, 32, 0, 7),
-           (0, -1, 0, 10, 3, 256, 32, 0, 7)],
-    "v8": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (31, -1, 0, 10, 3, 256, 32, 0, 7), (31, -1, 0, 10, 3, 256, 32, 0, 8),
-           (8, -1, -1, 10, 3, 256, 32, 0, 8)],
-    "k8": [(31, -1, 0, 10, 3, 256, 32, 0, 0), (31, -1, 0, 10, 3, 256, 32, 0, 8)],
+    "v8": [(31, -1, 0, 10, 3, 256, 32, 0, 5), (31, -1, 0, 10, 3, 256, 32, 0, 8), (8, -1, -1, 10, 3, 256, 32, 0, 8)],
+    "k8": [(31, -1, 0, 10, 3, 256, 32, 0, 5), (31, -1, 0, 10, 3, 256, 32, 0, 8)],
     "sweep": [(0, -1, 0, 10, 0), (64, -1, 0, 10, 0), (256, -1, 0, 10, 0), (1024, -1, 0, 10, 0), (31, -1, 0, 10, 0)],
 }
 

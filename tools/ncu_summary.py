@@ -37,7 +37,7 @@ def kernel_sha16() -> str:
 
     csrc = Path(__file__).resolve().parents[1] / "paper_1606_07822_b200" / "csrc"
     h = hashlib.sha256()
-    for name in ("cg_hogwild.cu", "cg_hog7.cu", "cg_device.cuh"):
+    for name in ("cg_hogwild.cu", "cg_hog8.cu", "cg_device.cuh"):
         if (csrc / name).exists():
             h.update((csrc / name).read_bytes())
     return h.hexdigest()[:16]
