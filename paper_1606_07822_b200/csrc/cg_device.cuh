@@ -175,6 +175,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                  "l"(src), "r"(bytes), "r"(smem_u32(mb))
                  : "memory");
 }
+// Shared -> global bulk reduction by the TMA unit (UBLKRED): dst[0..bytes) += src[0..bytes)
+// as f32 adds at L2, one instruction per row instead of one REDG per lane and 16 bytes.
+// Tracked by the issuing thread's bulk async-group (bulk_commit / bulk_wait_read).
+__device__ __forceinline__ void bulk_red_add_f32(float* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Waits until the sources of this thread's bulk groups (all but the newest N) have been read.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 // Orders this thread's generic-proxy shared-memory writes before later bulk copies.
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

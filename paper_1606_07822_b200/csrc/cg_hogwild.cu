@@ -33,6 +33,9 @@
 #ifndef CG_T2_READ
 #define CG_T2_READ 0  // 0: warps read the L2-tier cached rows flushed state (write-combining); 1: + their CTA pending delta
 #endif
+#ifndef CG_H_BULKRED
+#define CG_H_BULKRED 1  // 1: a batch's h rows leave shared memory by bulk reductions (TMA unit, UBLKRED); 0: REDG per lane
+#endif
 #ifndef CG_STAGE_BULK
 #define CG_STAGE_BULK 1  // 1: rows staged by bulk copies (TMA unit, UBLKCP); 0: cp.async (LDGSTS)
 #endif
@@ -507,6 +510,10 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog5_kernel(HogArgs a) {
                         }
                     }
                 }
+                if constexpr (CG_H_BULKRED) {  // the previous batch's h rows have left Hs
+                    bulk_wait_read<0>();
+                    __syncwarp();
+                }
                 for (int i = 0; i < nb; ++i) {
 #pragma unroll
                     for (int k = 0; k < DCH; ++k) {
@@ -693,7 +700,18 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog5_kernel(HogArgs a) {
                 }
                 __syncwarp();
                 // the contexts' rows move once, by their accumulated h (trainer.hpp:173)
+                if constexpr (CG_H_BULKRED) {
+                    // one bulk reduction per context row, issued by lane i for row i: the TMA
+                    // unit adds the whole row at L2 (no per-lane REDG); Hs is reused once
+                    // the reads have completed (bulk_wait_read above)
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane < nb && !((hot_ctx >> lane) & 1u))
+                        bulk_red_add_f32(a.syn0 + static_cast<size_t>(xid) * d4 * 4, Hs + lane * d4, row_bytes);
+                    bulk_commit();
+                }
                 for (int i = 0; i < nb; ++i) {
+                    if (CG_H_BULKRED && !(CTX && ((hot_ctx >> i) & 1u))) continue;
                     const int x = __shfl_sync(kFull, xid, i);
                     if (CTX && ((hot_ctx >> i) & 1u)) {  // merge into the CTA's cached delta
                         touched_cache = true;
@@ -736,6 +754,7 @@ __global__ void __launch_bounds__(WORKERS * 32, 1) hog5_kernel(HogArgs a) {
             }
         }
     }
+    if constexpr (CG_H_BULKRED) bulk_wait_read<0>();  // shared memory outlives the last bulk reductions
     int last = 0;
     if (lane == 0) {
         atomicAdd(a.counters + 1, n_pairs);

@@ -43,6 +43,7 @@ def main():
     p.add_argument("--eval-prefix", type=int, default=100_000_000, help="tokens the evaluation pairs are drawn from")
     p.add_argument("--ref-tokens", type=int, default=20_000_000, help="reference sample per K (0 = skip)")
     p.add_argument("--out", default="")
+    p.add_argument("--kernel", type=int, default=0, help="K1 version (cg_tuning.kernel; 0 = default)")
     a = p.parse_args()
 
     import torch
@@ -64,6 +65,8 @@ def main():
         cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
                               cache_nodes=k, seed=c.seed, mode="hogwild")
         sess = api.Session(vocab, tree, sel, cfg)
+        if a.kernel:
+            sess.tune(kernel=a.kernel)
         if isinstance(ids, np.ndarray):
             sess.upload_ids(ids)
         else:
@@ -88,7 +91,7 @@ def main():
         row = {"config": a.config, "k": k, "cached_rows_per_cta": e.cached_rows, "smem_rows": e.smem_rows,
                "l2_tier_rows": e.cached_rows - e.smem_rows, "floor_rows": e.floor_rows,
                "flush_centers": e.flush_centers, "worker_warps": e.worker_warps,
-               "ctx_batch": e.ctx_batch, "blocks": e.blocks, "tokens": T, "pairs": int(e.pairs), "steps": int(e.steps),
+               "ctx_batch": e.ctx_batch, "blocks": e.blocks, "kernel": e.kernel, "tokens": T, "pairs": int(e.pairs), "steps": int(e.steps),
                "k1_ms": kmed, "pass_ms_wall": float(np.median(ms)), "words_per_s_k1": T / (kmed / 1e3),
                "words_per_s_pass": T / (float(np.median(ms)) / 1e3),
                "algorithmic_gbs": 4.0 * c.dim * (2.0 * e.steps + 2.0 * e.pairs) / (kmed / 1e3) / 1e9,
