@@ -961,7 +961,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // v8 (tensor cores) unless the caller asked for v5 (FP32 FMA) or the rows are too wide
             auto plan_tc = [&](int32_t rows, int32_t ctx) {
                 return s->tune.kernel != 5 && cgk::hog8_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block,
-                                                             s->tune.centers_per_warp, n, s->max_depth, &g);
+                                                             s->tune.centers_per_warp, n, s->max_depth, s->cfg.window, &g);
             };
             bool v8 = plan_tc(std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0);
             const double inflight =

@@ -19,23 +19,33 @@
 // to nearest (TF32's operand precision); the fp32 model in HBM is unchanged and every sum
 // is fp32; the sigmoid is the reference's 1000-bucket table (bucket width 0.012), far
 // coarser than the operand rounding. fp16 staging halves a warp's shared memory against
-// fp32 (12 warps per SM at D 200, 8 at D 300, where fp32-staged TF32 operands left 6 and 5:
-// v7, measured slower than v5 for that reason and removed). Staging is pipelined: cp.async
-// lands each row in a slot of the warp's fp32 ring (4 rows in flight, one commit group per
-// row) and each lane converts the chunks it copied. Every fragment load is one ldmatrix --
+// fp32 (fp32-staged TF32 operands left 6 and 5 warps per SM at D 200 / 300: v7, measured
+// slower than v5 for that reason and removed). Staging goes through registers: every lane
+// loads its 16-byte chunks of kStage rows at once (ld.global.cg, coherent with the rows'
+// red.global updates at L2), converts them to half2 pairs and stores them -- no fp32 ring in
+// shared memory, which is what bounds the warps per SM. A warp holds min(16, 2W) context
+// rows and `urows` path rows; tile rows beyond them are read from one all-zero row the CTA
+// shares (ldmatrix takes a row address per lane). Every fragment load is one ldmatrix --
 // m8n8.x4 for the row-major operands, .trans for U as H's B, G^T as dU's A and V as dU's B;
 // row strides of 8 (mod 16) halves put the eight 16-byte rows of each matrix in distinct
 // banks.
 //
-// H and dU leave straight from the accumulator fragments with red.global.add.v2.f32 (no lost
-// updates, predicated instead of branched). The per-CTA node cache (NodeCache,
-// trainer.hpp:75-138): the K cached syn1 rows and the most frequent words' syn0 rows take
-// their updates in CTA-private delta rows in L2 (`tier2`), which the flush drains by atomic
-// exchange and adds to the model scaled per row; warps read a cached row's flushed state
-// (write-combining: a CTA's own pending delta joins the row at its flush, like every other
-// CTA's).
+// H and dU leave straight from the accumulator fragments with red.global.add.v2.f32 (no
+// lost updates). ptxas never predicates a REDG: a lane-divergent guard costs BSSY + BRA
+// + BSYNC around each one (29% of the stall samples of the first v8, which guarded every
+// REDG per lane). Here an 8-row group of the tile with no real row is skipped by a test the
+// compiler knows to be warp-uniform (template parameters HI / FULL), and only the lanes of
+// the padding rows inside a partly filled group branch. (Sending the padding rows' zeros to
+// a scratch row instead, branch-free, measured 16% slower, and pairing lanes by shuffle for
+// 16-byte REDGs 4% slower: C5 2775 and 2502 ms against 2398.) The per-CTA
+// node cache (NodeCache, trainer.hpp:75-138): the K cached syn1 rows and the most frequent
+// words' syn0 rows take their updates in CTA-private delta rows in L2 (`tier2`), which the
+// flush drains by atomic exchange and adds to the model scaled per row; warps read a cached
+// row's flushed state (write-combining: a CTA's own pending delta joins the row at its
+// flush, like every other CTA's).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include <cuda_fp16.h>
 
@@ -47,8 +57,13 @@ namespace {
 
 using namespace cgdev;
 
-constexpr int kVRows = 16;     // context rows per batch: M of one mma tile
+constexpr int kTileRows = 16;  // M of one mma tile: context rows per batch
 constexpr int kGhStride = 40;  // fp16 G scratch [16 contexts][32 path rows], 80-byte rows
+#ifndef CG_K8_STAGE3
+#define CG_K8_STAGE3 6
+#endif
+// rows a lane has in flight (registers) while staging, by 16-byte chunks per lane and row
+__host__ __device__ constexpr int k8_stage(int dch) { return dch >= 3 ? CG_K8_STAGE3 : 4; }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const __half* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -65,11 +80,12 @@ __device__ __forceinline__ void mma_f16(float (&c)[4], const uint32_t (&a)[4], u
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// red.global.add.v2.f32 under a predicate (no branch around it)
-__device__ __forceinline__ void red_add2_if(bool pred, float* p, float x, float y) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q red.global.add.v2.f32 [%0], {%1, %2};\n\t}" ::"l"(p),
-                 "f"(x), "f"(y), "r"(static_cast<unsigned>(pred))
-                 : "memory");
+// red.global.add.v2.f32 (REDG.E.ADD.F32x2) into a model row; a null row is a padding row of
+// the tile: its lanes branch around the REDG (ptxas never predicates one), which costs less
+// than sending their zeros to L2 (measured: C5 2386 ms against 2775 ms with a scratch row).
+__device__ __forceinline__ void red_add2(float* row, int col, float x, float y) {
+    if (row == nullptr) return;
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(row + col), "f"(x), "f"(y) : "memory");
 }
 __device__ __forceinline__ uint32_t half2_bits(float a, float b) {
     const __half2 h = __floats2half2_rn(a, b);
@@ -79,20 +95,21 @@ __device__ __forceinline__ uint32_t half2_bits(float a, float b) {
 // fp16 row stride (halves) for rows of dp floats: dp rounded up to 16 (the mma K step),
 // plus 8 -- 8 (mod 16) halves, an odd number of 16-byte chunks.
 __host__ __device__ constexpr int k8_stride(int dp) { return (dp + 15) / 16 * 16 + 8; }
-constexpr int kRing = 4;  // fp32 rows in flight per warp while staging
-// Per-warp bytes: G scratch | V (kVRows rows) | U (urows rows) | codes (32 ints) | fp32 ring
-// (kRing rows of dp floats: cp.async lands rows there, lanes convert them to fp16).
-__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int urows, int dp) {
-    return static_cast<uint32_t>(kVRows * kGhStride * 2 + (kVRows + urows) * ssh * 2 + 32 * 4 + kRing * dp * 4);
+// Per-warp bytes: G scratch | V (vrows context rows) | U (urows path rows) | codes (32 ints).
+__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int vrows, int urows) {
+    return static_cast<uint32_t>(kTileRows * kGhStride * 2 + (vrows + urows) * ssh * 2 + 32 * 4);
+}
+// Bytes ahead of the warps' regions: sigmoid table | touched-row bitmap | the all-zero row.
+__host__ __device__ constexpr uint32_t k8_fixed_bytes(int ssh, int cache_rows) {
+    return 4096u + ((static_cast<uint32_t>((cache_rows + 31) / 32) * 4u + 127u) & ~127u) +
+           ((static_cast<uint32_t>(ssh) * 2u + 127u) & ~127u);
 }
 
 // S = V U^T for NP pairs of 8-row n-tiles over K16 k-steps of 16 columns. The A fragment of
-// each k-step is one ldmatrix.x4 of V; the B fragments of two n-tiles one ldmatrix.x4 of U.
+// each k-step is one ldmatrix.x4 of V (pa: this lane's row of the 16 x 16 tile); the B
+// fragments of two n-tiles one ldmatrix.x4 of U (pb[np]: this lane's row of pair np).
 template <int NP, int K16>
-__device__ __forceinline__ void s_phase(const __half* V, const __half* U, int ssh, int k16, int lane, float (&acc)[4][4]) {
-    const int m = lane >> 3, rr = lane & 7;
-    const __half* pa = V + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
-    const __half* pb = U + (rr + 8 * (m >> 1)) * ssh + 8 * (m & 1);
+__device__ __forceinline__ void s_phase(const __half* pa, const __half* const (&pb)[2], int k16, float (&acc)[4][4]) {
     const int n16 = K16 > 0 ? K16 : k16;
 #pragma unroll 2
     for (int ks = 0; ks < n16; ++ks) {
@@ -101,23 +118,23 @@ __device__ __forceinline__ void s_phase(const __half* V, const __half* U, int ss
 #pragma unroll
         for (int np = 0; np < NP; ++np) {
             uint32_t b[4];
-            ldsm_x4(b, pb + 16 * np * ssh + 16 * ks);
+            ldsm_x4(b, pb[np] + 16 * ks);
             mma_f16(acc[2 * np], a, b[0], b[1]);
             mma_f16(acc[2 * np + 1], a, b[2], b[3]);
         }
     }
 }
 
-// H = G U over KS k-steps of 16 path rows; each pair of 8-column tiles goes to the context
-// rows g, g + 8 (columns below dp only).
-template <int KS, int K16>
-__device__ __forceinline__ void h_phase(const __half* GH, const __half* U, int ssh, int k16, int dp, int lane, float* p0,
-                                        float* p1, bool w0, bool w1) {
+// H = G U over KS k-steps of 16 path rows (pb[kk]: this lane's U row of k-step kk); each pair
+// of 8-column tiles goes to the context rows g (p0) and, when the batch has more than 8
+// contexts (HI), g + 8 (p1). A padding context has a null row.
+template <int KS, int K16, bool HI>
+__device__ __forceinline__ void h_phase(const __half* GH, const __half* const (&pb)[2], int k16, int dp, int lane, float* p0,
+                                        float* p1) {
     const int m = lane >> 3, rr = lane & 7, t = lane & 3;
     uint32_t a[KS][4];
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) ldsm_x4(a[kk], GH + (rr + 8 * (m & 1)) * kGhStride + 16 * kk + 8 * (m >> 1));
-    const __half* pb = U + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
     const int n16 = K16 > 0 ? K16 : k16;
 #pragma unroll 2
     for (int np = 0; np < n16; ++np) {
@@ -125,42 +142,49 @@ __device__ __forceinline__ void h_phase(const __half* GH, const __half* U, int s
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
             uint32_t b[4];
-            ldsm_x4_t(b, pb + 16 * kk * ssh + 16 * np);
+            ldsm_x4_t(b, pb[kk] + 16 * np);
             mma_f16(c0, a[kk], b[0], b[1]);
             mma_f16(c1, a[kk], b[2], b[3]);
         }
-        const int d0 = 16 * np + 2 * t, d1 = d0 + 8;
-        red_add2_if(w0, p0 + d0, c0[0], c0[1]);
-        red_add2_if(w1, p1 + d0, c0[2], c0[3]);
-        red_add2_if(w0 && d1 < dp, p0 + d1, c1[0], c1[1]);
-        red_add2_if(w1 && d1 < dp, p1 + d1, c1[2], c1[3]);
+        const int d0 = 16 * np + 2 * t;
+        const bool second = 16 * np + 8 < dp;  // warp-uniform: dp is a multiple of 8
+        red_add2(p0, d0, c0[0], c0[1]);
+        if (second) red_add2(p0, d0 + 8, c1[0], c1[1]);
+        if constexpr (HI) {
+            red_add2(p1, d0, c0[2], c0[3]);
+            if (second) red_add2(p1, d0 + 8, c1[2], c1[3]);
+        }
     }
 }
 
-// dU = G^T V for MT m-tiles of 16 path rows (one k-step: the batch's 16 contexts).
-template <int MT, int K16>
-__device__ __forceinline__ void u_phase(const __half* GH, const __half* V, int ssh, int k16, int dp, int lane,
-                                        float* const (&pr)[4], const bool (&pw)[4]) {
+// dU = G^T V for MT m-tiles of 16 path rows (one k-step: the batch's 16 contexts; pb: this
+// lane's V row). pr[e]: the row g + 8 e of this lane (null for padding rows); FULL: the
+// last 8-row group of the MT tiles holds a real path row.
+template <int MT, int K16, bool FULL>
+__device__ __forceinline__ void u_phase(const __half* GH, const __half* pb, int k16, int dp, int lane,
+                                        float* const (&pr)[4]) {
     const int m = lane >> 3, rr = lane & 7, t = lane & 3;
     uint32_t a[MT][4];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) ldsm_x4_t(a[mt], GH + (rr + 8 * (m >> 1)) * kGhStride + 16 * mt + 8 * (m & 1));
-    const __half* pb = V + (rr + 8 * (m & 1)) * ssh + 8 * (m >> 1);
     const int n16 = K16 > 0 ? K16 : k16;
 #pragma unroll 2
     for (int np = 0; np < n16; ++np) {
         uint32_t b[4];
         ldsm_x4_t(b, pb + 16 * np);
-        const int d0 = 16 * np + 2 * t, d1 = d0 + 8;
+        const int d0 = 16 * np + 2 * t;
+        const bool second = 16 * np + 8 < dp;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
             mma_f16(c0, a[mt], b[0], b[1]);
             mma_f16(c1, a[mt], b[2], b[3]);
-            red_add2_if(pw[2 * mt], pr[2 * mt] + d0, c0[0], c0[1]);
-            red_add2_if(pw[2 * mt + 1], pr[2 * mt + 1] + d0, c0[2], c0[3]);
-            red_add2_if(pw[2 * mt] && d1 < dp, pr[2 * mt] + d1, c1[0], c1[1]);
-            red_add2_if(pw[2 * mt + 1] && d1 < dp, pr[2 * mt + 1] + d1, c1[2], c1[3]);
+            red_add2(pr[2 * mt], d0, c0[0], c0[1]);
+            if (second) red_add2(pr[2 * mt], d0 + 8, c1[0], c1[1]);
+            if (FULL || mt + 1 < MT) {
+                red_add2(pr[2 * mt + 1], d0, c0[2], c0[3]);
+                if (second) red_add2(pr[2 * mt + 1], d0 + 8, c1[2], c1[3]);
+            }
         }
     }
 }
@@ -173,39 +197,53 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     constexpr int K16 = D4 > 0 ? (4 * D4 + 15) / 16 : 0;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int warps = blockDim.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
+    const int g = lane >> 2;
     const int d4 = D4 > 0 ? D4 : a.d4;
     const int dp = 4 * d4, k16 = (dp + 15) / 16;
     const int ssh = D4 > 0 ? k8_stride(4 * D4) : a.smem_stride;
-    const int UR = a.urows;
+    const int UR = a.urows, VR = a.ctx_batch;
     const int K = a.cache_rows, K0 = a.ctx_cache_rows;
     const int nwords = (K + 31) >> 5;
     unsigned char* base = k8_raw + ((128u - (smem_u32(k8_raw) & 127u)) & 127u);
     float* sig = reinterpret_cast<float*>(base);
     unsigned* touch = reinterpret_cast<unsigned*>(base + 4096);
-    unsigned char* wbase = base + 4096 + ((nwords * 4 + 127) & ~127);
-    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, UR, dp);
+    unsigned char* wbase = base + k8_fixed_bytes(ssh, K);
+    const __half* zrow = reinterpret_cast<const __half*>(wbase - ((static_cast<uint32_t>(ssh) * 2u + 127u) & ~127u));
+    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, VR, UR);
     __half* GH = reinterpret_cast<__half*>(wp);
-    __half* V = GH + kVRows * kGhStride;
-    __half* U = V + kVRows * ssh;
+    __half* V = GH + kTileRows * kGhStride;
+    __half* U = V + VR * ssh;
     int* codes = reinterpret_cast<int*>(U + UR * ssh);
-    float* ring = reinterpret_cast<float*>(codes + 32);
     float* t2 = a.tier2 ? a.tier2 + static_cast<size_t>(blockIdx.x) * static_cast<size_t>(K + K0) * dp : nullptr;
     float* t2c = t2 ? t2 + static_cast<size_t>(K) * dp : nullptr;
+    float* const scr = nullptr;  // the row pointer of a padding tile row
     __shared__ int s_done;
     __shared__ unsigned s_merged;
 
     for (int i = tid; i < 1000; i += blockDim.x) sig[i] = a.sigmoid[i];
     for (int i = tid; i < nwords; i += blockDim.x) touch[i] = 0u;
-    {  // staging zeroed once: the columns past a row and the padded rows stay finite
-        const int n = static_cast<int>(warps * k8_warp_bytes(ssh, UR, dp) / 16);
-        for (int i = tid; i < n; i += blockDim.x) reinterpret_cast<uint4*>(wbase)[i] = make_uint4(0u, 0u, 0u, 0u);
+    {  // zero row and staging zeroed once: the columns past a row and stale rows stay finite
+        uint4* z = reinterpret_cast<uint4*>(const_cast<__half*>(zrow));
+        const int n = static_cast<int>((((static_cast<uint32_t>(ssh) * 2u + 127u) & ~127u) +
+                                        warps * k8_warp_bytes(ssh, VR, UR)) / 16);
+        for (int i = tid; i < n; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (tid == 0) {
         s_done = 0;
         s_merged = 0;
     }
     __syncthreads();
+
+    // this lane's ldmatrix rows (tile rows past the staged ones read the zero row)
+    const int lm = lane >> 3, lr = lane & 7;
+    auto v_row = [&](int r) { return r < VR ? V + r * ssh : zrow; };
+    auto u_row = [&](int r) { return r < UR ? U + r * ssh : zrow; };
+    const __half* pa_s = v_row(lr + 8 * (lm & 1)) + 8 * (lm >> 1);                       // S: A = V
+    const __half* pb_s[2] = {u_row(lr + 8 * (lm >> 1)) + 8 * (lm & 1),                   // S: B = U
+                             u_row(16 + lr + 8 * (lm >> 1)) + 8 * (lm & 1)};
+    const __half* pb_h[2] = {u_row(lr + 8 * (lm & 1)) + 8 * (lm >> 1),                   // H: B = U (trans)
+                             u_row(16 + lr + 8 * (lm & 1)) + 8 * (lm >> 1)};
+    const __half* pb_u = v_row(lr + 8 * (lm & 1)) + 8 * (lm >> 1);                       // dU: B = V (trans)
 
     // ---- the CTA's cache flush: the touched rows' pending deltas (all of them at the end)
     // are taken with an atomic exchange and added to the model scaled per row.
@@ -246,38 +284,37 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
         __threadfence();  // the other SMs see this flush before the CTA's next one
     };
 
-    // rows -> fp16 in shared memory, pipelined: cp.async (LDGSTS, through L2 like the rows'
-    // red.global updates) lands each row in a slot of the warp's fp32 ring, one commit group
-    // per row, kRing rows in flight; a lane converts exactly the 16-byte chunks it copied
-    // (so no warp barrier is needed) to half2 pairs (round to nearest) as each row lands.
+    // rows -> fp16 in shared memory through registers: kStage rows in flight per lane
+    // (ld.global.cg: through L2, like the rows' red.global updates), each lane converting
+    // the 16-byte chunks it loaded to half2 pairs (round to nearest).
     auto stage_rows = [&](int nrows, auto&& src_of, auto&& dst_of) {
-        auto issue = [&](int r) {
-            if (r < nrows) {
-                const float* src = src_of(r);
-                float* slot = ring + (r % kRing) * dp;
+        constexpr int kStage = k8_stage(DCH);
+        for (int r0 = 0; r0 < nrows; r0 += kStage) {
+            float4 buf[kStage][DCH];
 #pragma unroll
-                for (int k = 0; k < DCH; ++k) {
-                    const int q = lane + 32 * k;
-                    if (k < DCH - 1 || q < d4) cp_async16(slot + 4 * q, src + 4 * q);
+            for (int r = 0; r < kStage; ++r) {
+                const float* src = src_of(min(r0 + r, nrows - 1));  // every lane takes part in the shuffles
+                if (r0 + r < nrows) {
+#pragma unroll
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        if (k < DCH - 1 || q < d4) buf[r][k] = ld_cg4(src + 4 * q);
+                    }
                 }
             }
-            asm volatile("cp.async.commit_group;" ::: "memory");  // empty past the last row
-        };
 #pragma unroll
-        for (int r = 0; r < kRing; ++r) issue(r);
-        for (int r = 0; r < nrows; ++r) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
-            const float* slot = ring + (r % kRing) * dp;
-            __half* d = dst_of(r);
+            for (int r = 0; r < kStage; ++r) {
+                if (r0 + r < nrows) {
+                    __half* d = dst_of(r0 + r);
 #pragma unroll
-            for (int k = 0; k < DCH; ++k) {
-                const int q = lane + 32 * k;
-                if (k < DCH - 1 || q < d4) {
-                    const float4 v = *reinterpret_cast<const float4*>(slot + 4 * q);
-                    *reinterpret_cast<uint2*>(d + 4 * q) = make_uint2(half2_bits(v.x, v.y), half2_bits(v.z, v.w));
+                    for (int k = 0; k < DCH; ++k) {
+                        const int q = lane + 32 * k;
+                        if (k < DCH - 1 || q < d4)
+                            *reinterpret_cast<uint2*>(d + 4 * q) =
+                                make_uint2(half2_bits(buf[r][k].x, buf[r][k].y), half2_bits(buf[r][k].z, buf[r][k].w));
+                    }
                 }
             }
-            issue(r + kRing);
         }
     };
 
@@ -314,8 +351,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
             const int n = static_cast<int>(hi - lo);
             if (n == 0) continue;
             bool touched_cache = false;
-            for (int q0 = 0; q0 < n; q0 += kVRows) {
-                const int nb = min(kVRows, n - q0);
+            for (int q0 = 0; q0 < n; q0 += VR) {
+                const int nb = min(VR, n - q0);
                 int xid = 0;
                 if (lane < nb) {
                     int64_t pos = lo + q0 + lane;
@@ -324,9 +361,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                 }
                 const unsigned hot_ctx = __ballot_sync(kFull, lane < nb && xid < K0);
                 const int x0 = __shfl_sync(kFull, xid, g), x1 = __shfl_sync(kFull, xid, (g + 8) & 31);
-                float* pc0 = ((hot_ctx >> g) & 1u ? t2c : a.syn0) + static_cast<size_t>(x0) * dp;
-                float* pc1 = ((hot_ctx >> (g + 8)) & 1u ? t2c : a.syn0) + static_cast<size_t>(x1) * dp;
-                const bool w0 = g < nb, w1 = g + 8 < nb;
+                // the context rows of this lane's accumulator rows g, g + 8 (null when padding)
+                float* pc0 = g < nb ? ((hot_ctx >> g) & 1u ? t2c : a.syn0) + static_cast<size_t>(x0) * dp : scr;
+                float* pc1 = g + 8 < nb ? ((hot_ctx >> (g + 8)) & 1u ? t2c : a.syn0) + static_cast<size_t>(x1) * dp : scr;
                 for (int jc = 0; jc < L; jc += UR) {
                     const int Lc = min(UR, L - jc);
                     const bool restage = q0 == 0 || L > UR;  // U is kept across the batches of one chunk
@@ -334,8 +371,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                     if (lane < Lc) code = a.path_code[p0 + jc + lane];
                     const int row = code >> 1;
                     __syncwarp();  // the previous chunk / batch is done with V, U and G
-                    // the batch's context rows (first chunk) and the chunk's path rows, as fp16
-                    {  // one pipeline: rows [0, nv) are context rows, then the chunk's path rows
+                    {  // the batch's context rows (first chunk) and the chunk's path rows, as fp16
                         const int nv = jc == 0 ? nb : 0, nu = restage ? Lc : 0;
                         stage_rows(
                             nv + nu,
@@ -352,8 +388,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                     float acc[4][4];
 #pragma unroll
                     for (int n2 = 0; n2 < 4; ++n2) acc[n2][0] = acc[n2][1] = acc[n2][2] = acc[n2][3] = 0.f;
-                    if (NP == 1) s_phase<1, K16>(V, U, ssh, k16, lane, acc);
-                    else s_phase<2, K16>(V, U, ssh, k16, lane, acc);
+                    if (NP == 1) s_phase<1, K16>(pa_s, pb_s, k16, acc);
+                    else s_phase<2, K16>(pa_s, pb_s, k16, acc);
+                    const int t = lane & 3;
 #pragma unroll
                     for (int n2 = 0; n2 < 4; ++n2) {
                         if (n2 >= 2 * NP) break;
@@ -370,20 +407,29 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                     }
                     __syncwarp();
                     // ---- H = G U -> the context rows (v += h, trainer.hpp:173) ----
-                    if (NP == 1) h_phase<1, K16>(GH, U, ssh, k16, dp, lane, pc0, pc1, w0, w1);
-                    else h_phase<2, K16>(GH, U, ssh, k16, dp, lane, pc0, pc1, w0, w1);
+                    if (NP == 1) {
+                        if (nb > 8) h_phase<1, K16, true>(GH, pb_h, k16, dp, lane, pc0, pc1);
+                        else h_phase<1, K16, false>(GH, pb_h, k16, dp, lane, pc0, pc1);
+                    } else {
+                        if (nb > 8) h_phase<2, K16, true>(GH, pb_h, k16, dp, lane, pc0, pc1);
+                        else h_phase<2, K16, false>(GH, pb_h, k16, dp, lane, pc0, pc1);
+                    }
                     // ---- dU = G^T V -> the path rows (syn1, or the CTA's delta of a cached row) ----
                     float* pr[4];
-                    bool pw[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int j = g + 8 * e;  // m-tile e / 2, rows g and g + 8
                         const int rj = __shfl_sync(kFull, row, j);
-                        pw[e] = j < Lc;
-                        pr[e] = (rj < K ? t2 : a.syn1) + static_cast<size_t>(rj) * dp;
+                        pr[e] = j < Lc ? (rj < K ? t2 : a.syn1) + static_cast<size_t>(rj) * dp : scr;
                     }
-                    if (NP == 1) u_phase<1, K16>(GH, V, ssh, k16, dp, lane, pr, pw);
-                    else u_phase<2, K16>(GH, V, ssh, k16, dp, lane, pr, pw);
+                    const bool full = ((Lc - 1) & 15) >= 8;  // the tiles' last 8-row group has a real row
+                    if (NP == 1) {
+                        if (full) u_phase<1, K16, true>(GH, pb_u, k16, dp, lane, pr);
+                        else u_phase<1, K16, false>(GH, pb_u, k16, dp, lane, pr);
+                    } else {
+                        if (full) u_phase<2, K16, true>(GH, pb_u, k16, dp, lane, pr);
+                        else u_phase<2, K16, false>(GH, pb_u, k16, dp, lane, pr);
+                    }
                     const bool cached = lane < Lc && row < K;
                     if (__any_sync(kFull, cached)) {
                         touched_cache = true;
@@ -417,31 +463,42 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     if (last && (K > 0 || K0 > 0)) flush_cache(true);
 }
 
-constexpr int kV8MaxWarps = 16;
-
-template <int DCH, int D4>
+template <int DCH, int WARPS, int D4>
 void launch8(const HogArgs& a, const HogGeometry& g, cudaStream_t s) {
-    auto k = hog8_kernel<DCH, kV8MaxWarps, D4>;
+    auto k = hog8_kernel<DCH, WARPS, D4>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(g.smem));
     k<<<g.blocks, g.warps * 32, g.smem, s>>>(a);
 }
 
+// Warps per CTA each staging width is compiled for (the launch bound sets the register cap:
+// 128 at 16 warps, 146 at 14, 204 at 10). Shared memory holds no more than these at the
+// benchmark widths anyway (D 200: 14 warps with 24 path rows; D 300: 10).
+constexpr int k8_max_warps(int dch) { return dch >= 3 ? 10 : dch == 2 ? 14 : 16; }
+
 }  // namespace
 
 bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
-               int max_depth, HogGeometry* g) {
+               int max_depth, int window, HogGeometry* g) {
     if (d4 > 96) return false;
     const int dp = 4 * d4;
     const int ssh = k8_stride(dp);
-    const int nwords = (cache_rows + 31) / 32;
-    const size_t fixed = 4096 + ((static_cast<size_t>(nwords) * 4 + 127) & ~size_t{127}) + 128;
+    const size_t fixed = k8_fixed_bytes(ssh, cache_rows) + 128;
     const size_t budget = 227 * 1024 - 1024;
-    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, ur, dp)); };
-    // Path rows staged per chunk: the deepest path when it fits in 32 rows, 16 where 32
-    // would leave fewer than 10 warps; a deeper path trains in chunks (contexts stay staged).
-    int urows = max_depth > 16 ? 32 : 16;
-    if (urows == 32 && warps_for(32) < 10) urows = 16;
-    int warps = std::min(kV8MaxWarps, warps_for(urows));
+    // context rows staged per batch: a full window when it fits the 16-row tile
+    const int vrows = std::min(kTileRows, std::max(2, 2 * window));
+    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, vrows, ur)); };
+    const int cap = k8_max_warps((d4 + 31) / 32);
+    // Path rows staged per chunk (a deeper path trains in chunks, its contexts staying
+    // staged; every chunk repeats the H phase): 16 when no path is deeper, else 24 when that
+    // keeps at least 8 warps on the SM (measured, K1 ms at 16 / 24 / 32 rows: C5 3109 / 2872 /
+    // 3053, C2 67.3 / 63.9 / 69.9, C4 914 / 881 / 934). CG_UROWS overrides (experiments).
+    int urows = 16;
+    if (max_depth > 16 && std::min(cap, warps_for(24)) >= 8) urows = 24;
+    if (const char* e = std::getenv("CG_UROWS")) {
+        const int v = std::atoi(e);
+        if (v == 16 || v == 24 || v == 32) urows = v;
+    }
+    int warps = std::min(cap, warps_for(urows));
     if (warps_override > 0) warps = std::min(warps, warps_override);
     if (warps < 1) return false;
     g->variant = 8;
@@ -450,12 +507,12 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     g->cache_rows = cache_rows;
     g->smem_rows = 0;
     g->ctx_rows = ctx_rows;
-    g->ctx_batch = kVRows;
+    g->ctx_batch = vrows;
     g->flusher = false;
     g->urows = urows;
     g->smem_stride = ssh;
     g->specialise = true;
-    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, urows, dp);
+    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, vrows, urows);
     g->cpw = cpw_override > 0 ? std::min(cpw_override, 32)
                               : (tokens / (static_cast<int64_t>(blocks) * warps) >= 2000 ? 16 : 8);
     return true;
@@ -467,21 +524,21 @@ void launch_hog8(const HogArgs& a0, const HogGeometry& g, cudaStream_t s) {
     a.smem_rows = 0;
     a.ctx_cache_rows = g.ctx_rows;
     a.centers_per_warp = g.cpw;
-    a.ctx_batch = kVRows;
+    a.ctx_batch = g.ctx_batch;
     a.flusher = 0;
     a.urows = g.urows;
     a.smem_stride = g.smem_stride;
     const int dch = (a.d4 + 31) / 32;
     switch (a.d4) {  // the benchmark row widths (D 100, 128, 200, 300 padded to 8 floats)
-        case 26: launch8<1, 26>(a, g, s); return;
-        case 32: launch8<1, 32>(a, g, s); return;
-        case 50: launch8<2, 50>(a, g, s); return;
-        case 76: launch8<3, 76>(a, g, s); return;
+        case 26: launch8<1, k8_max_warps(1), 26>(a, g, s); return;
+        case 32: launch8<1, k8_max_warps(1), 32>(a, g, s); return;
+        case 50: launch8<2, k8_max_warps(2), 50>(a, g, s); return;
+        case 76: launch8<3, k8_max_warps(3), 76>(a, g, s); return;
         default: break;
     }
-    if (dch == 1) launch8<1, 0>(a, g, s);
-    else if (dch == 2) launch8<2, 0>(a, g, s);
-    else launch8<3, 0>(a, g, s);
+    if (dch == 1) launch8<1, k8_max_warps(1), 0>(a, g, s);
+    else if (dch == 2) launch8<2, k8_max_warps(2), 0>(a, g, s);
+    else launch8<3, k8_max_warps(3), 0>(a, g, s);
 }
 
 }  // namespace cgk

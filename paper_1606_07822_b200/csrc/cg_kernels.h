@@ -141,7 +141,7 @@ struct HogGeometry {
     int cpw;          // centers per ticket
     int cache_rows;   // K (both tiers)
     int smem_rows;    // S
-    int ctx_batch;    // contexts staged per warp
+    int ctx_batch;    // contexts staged per warp (v8: min(16, 2W) rows of the 16-row tile)
     int variant;      // 8 = v8 (tensor cores); 1..3 = v5 (FP32, float4 chunks per lane); 0 = generic
     bool specialise;  // use the row-width-specialised instantiation when there is one
     bool flusher;     // one extra (flusher) warp; only when registers leave room for it
@@ -168,7 +168,7 @@ void launch_hogwild(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 // m16n8k16 f16, fp32 accumulation) from fp16-staged rows. Returns false where it does not
 // apply (rows wider than 384 floats, or no warp fits).
 bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_override, int cpw_override, int64_t tokens,
-               int max_depth, HogGeometry* g);
+               int max_depth, int window, HogGeometry* g);
 void launch_hog8(const HogArgs& a, const HogGeometry& g, cudaStream_t s);
 
 // ---------------- evaluation (cg_eval.cu) -----------------------------------------

@@ -66,6 +66,11 @@ def main():
         nbytes = d.numel() * 4
         row = d.view(-1, (c.dim + 7) // 8 * 8)
         touched = int((row != 0).any(dim=1).sum().item())
+        # the first apply of an (N, interval) pair builds and uploads the per-row scale table
+        # on the host (cached afterwards): time the steady-state apply
+        s.sync_apply(2, sw)
+        s.sync_delta_tensor()
+        torch.cuda.synchronize()
         ev[2].record(stream)
         s.sync_apply(2, sw)
         ev[3].record(stream)
