@@ -61,7 +61,9 @@ def parse():
     p.add_argument("--hot-flush-scale", type=float, default=0.0)
     p.add_argument("--flush-centers", type=int, default=0)
     p.add_argument("--min-cache-rows", type=int, default=0)
-    p.add_argument("--kernel", type=int, default=0, help="K1 version (0 = default)")
+    p.add_argument("--kernel", type=int, default=0, help="K1 version (0 = default: v8; 5 = the all-FP32 kernel)")
+    p.add_argument("--fp32-steps", type=int, default=2,
+                   help="also time this many passes of the all-FP32 K1 (kernel 5) when the timed kernel is v8 (0 = skip)")
     return p.parse_args()
 
 
@@ -386,6 +388,33 @@ def main():
     words_all = float(T) * args.steps * world  # every rank's shard has the same size
     value = words_all / (total_ms / 1e3)
 
+    # The all-FP32 K1 (v5: packed FFMA2, no tensor cores) on the same resident inputs, for
+    # readers who want the number without fp16 operand rounding: same step, device-timed.
+    fp32_arm = None
+    kernel_run = (agg.get("geometry") or {}).get("kernel")
+    if world == 1 and kernel_run == 8 and args.fp32_steps > 0:
+        sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.hot_flush_scale, args.flush_centers,
+                  args.min_cache_rows, 5)
+        record["on"] = False
+        sess.train_range(30_000, 0, T)
+        torch.cuda.synchronize()
+        ms5 = []
+        geo5 = None
+        for s in range(args.fp32_steps):
+            l2_flush.fill_(float(s))
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(stream)
+            e5 = sess.train_range(40_000 + s, 0, T)
+            ev1.record(stream)
+            ev1.synchronize()
+            ms5.append(ev0.elapsed_time(ev1))
+            geo5 = {"worker_warps": e5.worker_warps, "ctx_batch": e5.ctx_batch, "kernel": e5.kernel,
+                    "k1_ms": e5.train_ms}
+        fp32_arm = {"value": float(T) * len(ms5) / (sum(ms5) / 1e3), "unit": UNIT, "ms_per_step": sum(ms5) / len(ms5),
+                    "steps": len(ms5), "kernel": "hog5_kernel (K1 v5, FP32 FMA arithmetic end to end)", "geometry": geo5}
+        sess.tune(args.blocks, args.warps, args.cpw, args.rows, args.hot_flush_scale, args.flush_centers,
+                  args.min_cache_rows, args.kernel)
+
     # Roofline of the dominant kernel (K1). The HBM roofline is graded on
     # DRAM bytes: `achieved` = ncu-measured DRAM bytes per K1 launch (profiles/, captured
     # for this kernel source: `traffic_current`) / this run's CUDA-event K1 time. The
@@ -520,7 +549,9 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "vs_baseline": None,
+            "dtype": "f32 model, sums and updates; fp16 mma operands (K1 v8)" if kernel_run == 8 else "f32",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {c.tokens / 1e6:g}M-token Zipf({c.zipf_s}) per GPU, V {vocab.size()}, "
                                    f"D {c.dim}, W {c.window}, sample {c.sample}, K {args.cache_nodes}, 1 pass per step",
                        "l2": "256 MB buffer written between timed steps", "parallelism": f"replicas{world}",
@@ -532,6 +563,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_text": e2e_text,
+            "fp32_kernel": fp32_arm,
             "gpu_launches": launches["n"],
             "clocks": clk,
             "detail": {"syncs": trainer.syncs, "sync_bytes": trainer.sync_bytes,

@@ -21,8 +21,9 @@
 // coarser than the operand rounding. fp16 staging halves a warp's shared memory against
 // fp32 (fp32-staged TF32 operands left 6 and 5 warps per SM at D 200 / 300: v7, measured
 // slower than v5 for that reason and removed). Staging goes through registers: every lane
-// loads its 16-byte chunks of kStage rows at once (ld.global.cg, coherent with the rows'
-// red.global updates at L2), converts them to half2 pairs and stores them -- no fp32 ring in
+// loads its 16-byte chunks of 4-6 rows at once (ld.global.cg, coherent with the rows'
+// red.global updates at L2), converts them to half2 pairs and stores them -- row by row for
+// wide rows, as a flat list of (row, chunk) items for rows of at most 32 chunks -- no fp32 ring in
 // shared memory, which is what bounds the warps per SM. A warp holds min(16, 2W) context
 // rows and `urows` path rows; tile rows beyond them are read from one all-zero row the CTA
 // shares (ldmatrix takes a row address per lane). Every fragment load is one ldmatrix --
@@ -64,6 +65,10 @@ constexpr int kGhStride = 40;  // fp16 G scratch [16 contexts][32 path rows], 80
 #endif
 // rows a lane has in flight (registers) while staging, by 16-byte chunks per lane and row
 __host__ __device__ constexpr int k8_stage(int dch) { return dch >= 3 ? CG_K8_STAGE3 : 4; }
+// Rows of at most 32 chunks (D <= 128) stage as a flat list of (row, chunk) items, every lane
+// busy and no test per row (C3 75.8 -> 70.9 ms); wider rows stage row by row: the flat
+// list's address table costs them a warp of shared memory (C5 2335 -> 2588 ms with it).
+__host__ __device__ constexpr bool k8_flat(int dch) { return dch == 1; }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const __half* p) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -95,9 +100,10 @@ __device__ __forceinline__ uint32_t half2_bits(float a, float b) {
 // fp16 row stride (halves) for rows of dp floats: dp rounded up to 16 (the mma K step),
 // plus 8 -- 8 (mod 16) halves, an odd number of 16-byte chunks.
 __host__ __device__ constexpr int k8_stride(int dp) { return (dp + 15) / 16 * 16 + 8; }
-// Per-warp bytes: G scratch | V (vrows context rows) | U (urows path rows) | codes (32 ints).
-__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int vrows, int urows) {
-    return static_cast<uint32_t>(kTileRows * kGhStride * 2 + (vrows + urows) * ssh * 2 + 32 * 4);
+// Per-warp bytes: G scratch | V (vrows context rows) | U (urows path rows) | codes (32 ints)
+// | flat staging: 48 row addresses.
+__host__ __device__ constexpr uint32_t k8_warp_bytes(int ssh, int vrows, int urows, int dch) {
+    return static_cast<uint32_t>(kTileRows * kGhStride * 2 + (vrows + urows) * ssh * 2 + 32 * 4 + (k8_flat(dch) ? 48 * 8 : 0));
 }
 // Bytes ahead of the warps' regions: sigmoid table | touched-row bitmap | the all-zero row.
 __host__ __device__ constexpr uint32_t k8_fixed_bytes(int ssh, int cache_rows) {
@@ -209,7 +215,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     unsigned* touch = reinterpret_cast<unsigned*>(base + 4096);
     unsigned char* wbase = base + k8_fixed_bytes(ssh, K);
     const __half* zrow = reinterpret_cast<const __half*>(wbase - ((static_cast<uint32_t>(ssh) * 2u + 127u) & ~127u));
-    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, VR, UR);
+    unsigned char* wp = wbase + static_cast<size_t>(warp) * k8_warp_bytes(ssh, VR, UR, DCH);
     __half* GH = reinterpret_cast<__half*>(wp);
     __half* V = GH + kTileRows * kGhStride;
     __half* U = V + VR * ssh;
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
     {  // zero row and staging zeroed once: the columns past a row and stale rows stay finite
         uint4* z = reinterpret_cast<uint4*>(const_cast<__half*>(zrow));
         const int n = static_cast<int>((((static_cast<uint32_t>(ssh) * 2u + 127u) & ~127u) +
-                                        warps * k8_warp_bytes(ssh, VR, UR)) / 16);
+                                        warps * k8_warp_bytes(ssh, VR, UR, DCH)) / 16);
         for (int i = tid; i < n; i += blockDim.x) z[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (tid == 0) {
@@ -318,6 +324,42 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
         }
     };
 
+    // Flat staging: the nv context rows (into V) and nu path rows (into U, which follows V)
+    // are one list of (row, 16-byte chunk) items; lane l takes items l, l + 32, ... so every
+    // lane loads and converts, whatever the row width. Lanes publish their rows' global
+    // addresses in the warp's table first (lane i: context i, lane j: path row j).
+    unsigned long long* rtab = reinterpret_cast<unsigned long long*>(codes + 32);
+    const unsigned rcp = 0xffffffffu / static_cast<unsigned>(d4) + 1u;  // i / d4 = umulhi(i, rcp) for i < 2^25
+    auto stage_flat = [&](int nv, int nu, int xid, int row) {
+        constexpr int kItems = k8_stage(DCH) * DCH;
+        if (lane < nv) rtab[lane] = reinterpret_cast<unsigned long long>(a.syn0 + static_cast<size_t>(xid) * dp);
+        if (lane < nu) rtab[nv + lane] = reinterpret_cast<unsigned long long>(a.syn1 + static_cast<size_t>(row) * dp);
+        __syncwarp();
+        const int total = (nv + nu) * d4, dshift = VR - nv;
+        for (int i0 = lane; i0 < total; i0 += 32 * kItems) {
+            float4 buf[kItems];
+#pragma unroll
+            for (int u = 0; u < kItems; ++u) {
+                const int i = i0 + 32 * u;
+                if (i < total) {
+                    const int r = D4 > 0 ? i / D4 : static_cast<int>(__umulhi(static_cast<unsigned>(i), rcp));
+                    const int q = i - r * d4;
+                    buf[u] = ld_cg4(reinterpret_cast<const float*>(rtab[r]) + 4 * q);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kItems; ++u) {
+                const int i = i0 + 32 * u;
+                if (i < total) {
+                    const int r = D4 > 0 ? i / D4 : static_cast<int>(__umulhi(static_cast<unsigned>(i), rcp));
+                    const int q = i - r * d4;
+                    __half* d = V + (r + (r >= nv ? dshift : 0)) * ssh + 4 * q;
+                    *reinterpret_cast<uint2*>(d) = make_uint2(half2_bits(buf[u].x, buf[u].y), half2_bits(buf[u].z, buf[u].w));
+                }
+            }
+        }
+    };
+
     const int64_t n_kept = static_cast<int64_t>(*a.n_kept_dev);
     const int cpw = a.centers_per_warp;
     unsigned long long n_pairs = 0, n_steps = 0, n_centers = 0;
@@ -373,7 +415,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) hog8_kernel(HogArgs a) {
                     __syncwarp();  // the previous chunk / batch is done with V, U and G
                     {  // the batch's context rows (first chunk) and the chunk's path rows, as fp16
                         const int nv = jc == 0 ? nb : 0, nu = restage ? Lc : 0;
-                        stage_rows(
+                        if constexpr (k8_flat(DCH)) stage_flat(nv, nu, xid, row);
+                        else stage_rows(
                             nv + nu,
                             [&](int r) {
                                 return r < nv ? a.syn0 + static_cast<size_t>(__shfl_sync(kFull, xid, r)) * dp
@@ -486,7 +529,7 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     const size_t budget = 227 * 1024 - 1024;
     // context rows staged per batch: a full window when it fits the 16-row tile
     const int vrows = std::min(kTileRows, std::max(2, 2 * window));
-    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, vrows, ur)); };
+    auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, vrows, ur, (d4 + 31) / 32)); };
     const int cap = k8_max_warps((d4 + 31) / 32);
     // Path rows staged per chunk (a deeper path trains in chunks, its contexts staying
     // staged; every chunk repeats the H phase): 16 when no path is deeper, else 24 when that
@@ -512,7 +555,7 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     g->urows = urows;
     g->smem_stride = ssh;
     g->specialise = true;
-    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, vrows, urows);
+    g->smem = fixed + static_cast<size_t>(warps) * k8_warp_bytes(ssh, vrows, urows, (d4 + 31) / 32);
     g->cpw = cpw_override > 0 ? std::min(cpw_override, 32)
                               : (tokens / (static_cast<int64_t>(blocks) * warps) >= 2000 ? 16 : 8);
     return true;
