@@ -11,8 +11,9 @@ Hogwild training (+ the replicas' delta sync at N > 1).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 Under torchrun each rank trains its own full-size shard (weak scaling) on its own GPU and
-sums the replicas' deltas with NCCL every --sync-words words per GPU (default 1M; 25M at
-C5, sized so the dense 2.4 GB delta all-reduce stays near 10% of the pass at N = 8).
+sums the replicas' deltas with NCCL every --sync-words words per GPU (default 1M; 50M at
+C5, sized so the dense 2.4 GB delta all-reduce stays under 10% of the pass at N = 8:
+20 syncs x ~9 ms against a 2.3 s pass).
 Rank 0 prints ONE JSON line. `--impl reference` times the reference's own CPU
 implementation (the reference headers compiled unchanged, oracle/_ref) on this host's
 cores on a bounded sample.
@@ -47,7 +48,7 @@ def parse():
     p.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--cache-nodes", type=int, default=31)
     p.add_argument("--sync-words", type=int, default=0,
-                   help="delta all-reduce interval per GPU at N > 1 (0 = 25M at C5, else 1M)")
+                   help="delta all-reduce interval per GPU at N > 1 (0 = 50M at C5, else 1M)")
     p.add_argument("--sync-mode", default="delta", choices=["delta", "average"])
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--e2e-text-max-tokens", type=int, default=20_000_000,
@@ -317,7 +318,7 @@ def main():
         sess.upload_ids_device(ids)
     model_t = sess.model_tensor() if world > 1 else None
     if not args.sync_words:
-        args.sync_words = 25_000_000 if args.config == "c5" else 1_000_000
+        args.sync_words = 50_000_000 if args.config == "c5" else 1_000_000
     l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     T = int(len(ids))
@@ -434,12 +435,15 @@ def main():
 
     src_sha = kernel_sha16()
     traffic = l2_traffic = None
+    ncu_pcts = {}
     traffic_current = False
     prof = ROOT / "profiles" / f"ncu_traffic_{args.config}.json"
     if prof.exists():
         try:
             tj = json.loads(prof.read_text())
             traffic, l2_traffic = tj.get("dram_bytes_per_launch"), tj.get("l2_bytes_per_launch")
+            ncu_pcts = {k: tj.get(k) for k in ("lts_throughput_pct", "l1tex_throughput_pct", "issue_active_pct",
+                                                "l2_hit_rate_pct") if tj.get(k) is not None}
             traffic_current = tj.get("kernel_sha16") == src_sha
         except Exception:
             traffic = l2_traffic = None
@@ -456,6 +460,9 @@ def main():
         "traffic_current": traffic_current, "kernel_sha16": src_sha,
         "dram_frac": dram_gbs / peak if dram_gbs else None,
         "l2_traffic": l2_traffic,
+        "l2": {"achieved_gbs": l2_traffic / (per_launch_ms / 1e3) / 1e9 if l2_traffic else None,
+               "ncu": ncu_pcts or None,
+               "note": "L2 bytes of the same ncu capture / this run's K1 time; ncu percentages are the capture's"},
         "algorithmic_bytes_per_launch": per_launch_bytes, "algorithmic_gbs": algorithmic_gbs,
         "algorithmic_gbs_over_hbm_peak": algorithmic_gbs / peak,
         "fp32": {"fma_per_launch": fma_per_launch, "achieved_tfma_s": fp32_achieved / 1e12,

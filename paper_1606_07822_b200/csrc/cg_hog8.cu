@@ -60,6 +60,14 @@ using namespace cgdev;
 
 constexpr int kTileRows = 16;  // M of one mma tile: context rows per batch
 constexpr int kGhStride = 40;  // fp16 G scratch [16 contexts][32 path rows], 80-byte rows
+#ifndef CG_K8_SWP
+#define CG_K8_SWP 0  // 1: the H and dU loops load the next tile's B fragment before this tile's mma
+#endif
+#ifndef CG_K8_UNROLL
+#define CG_K8_UNROLL 2
+#endif
+#define CG_PRAGMA(x) _Pragma(#x)
+#define CG_UNROLL(n) CG_PRAGMA(unroll n)
 #ifndef CG_K8_STAGE3
 #define CG_K8_STAGE3 6
 #endif
@@ -117,7 +125,7 @@ __host__ __device__ constexpr uint32_t k8_fixed_bytes(int ssh, int cache_rows) {
 template <int NP, int K16>
 __device__ __forceinline__ void s_phase(const __half* pa, const __half* const (&pb)[2], int k16, float (&acc)[4][4]) {
     const int n16 = K16 > 0 ? K16 : k16;
-#pragma unroll 2
+CG_UNROLL(CG_K8_UNROLL)
     for (int ks = 0; ks < n16; ++ks) {
         uint32_t a[4];
         ldsm_x4(a, pa + 16 * ks);
@@ -142,9 +150,28 @@ __device__ __forceinline__ void h_phase(const __half* GH, const __half* const (&
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) ldsm_x4(a[kk], GH + (rr + 8 * (m & 1)) * kGhStride + 16 * kk + 8 * (m >> 1));
     const int n16 = K16 > 0 ? K16 : k16;
-#pragma unroll 2
+#if CG_K8_SWP
+    uint32_t bn[KS][4];
+#pragma unroll
+    for (int kk = 0; kk < KS; ++kk) ldsm_x4_t(bn[kk], pb[kk]);
+#endif
+CG_UNROLL(CG_K8_UNROLL)
     for (int np = 0; np < n16; ++np) {
         float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
+#if CG_K8_SWP
+        uint32_t b[KS][4];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) b[kk][e] = bn[kk][e];
+            if (np + 1 < n16) ldsm_x4_t(bn[kk], pb[kk] + 16 * (np + 1));
+        }
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            mma_f16(c0, a[kk], b[kk][0], b[kk][1]);
+            mma_f16(c1, a[kk], b[kk][2], b[kk][3]);
+        }
+#else
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
             uint32_t b[4];
@@ -152,6 +179,7 @@ __device__ __forceinline__ void h_phase(const __half* GH, const __half* const (&
             mma_f16(c0, a[kk], b[0], b[1]);
             mma_f16(c1, a[kk], b[2], b[3]);
         }
+#endif
         const int d0 = 16 * np + 2 * t;
         const bool second = 16 * np + 8 < dp;  // warp-uniform: dp is a multiple of 8
         red_add2(p0, d0, c0[0], c0[1]);
@@ -174,10 +202,20 @@ __device__ __forceinline__ void u_phase(const __half* GH, const __half* pb, int 
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) ldsm_x4_t(a[mt], GH + (rr + 8 * (m >> 1)) * kGhStride + 16 * mt + 8 * (m & 1));
     const int n16 = K16 > 0 ? K16 : k16;
-#pragma unroll 2
+#if CG_K8_SWP
+    uint32_t bn[4];
+    ldsm_x4_t(bn, pb);
+#endif
+CG_UNROLL(CG_K8_UNROLL)
     for (int np = 0; np < n16; ++np) {
         uint32_t b[4];
+#if CG_K8_SWP
+#pragma unroll
+        for (int e = 0; e < 4; ++e) b[e] = bn[e];
+        if (np + 1 < n16) ldsm_x4_t(bn, pb + 16 * (np + 1));
+#else
         ldsm_x4_t(b, pb + 16 * np);
+#endif
         const int d0 = 16 * np + 2 * t;
         const bool second = 16 * np + 8 < dp;
 #pragma unroll
@@ -539,7 +577,7 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     if (max_depth > 16 && std::min(cap, warps_for(24)) >= 8) urows = 24;
     if (const char* e = std::getenv("CG_UROWS")) {
         const int v = std::atoi(e);
-        if (v == 16 || v == 24 || v == 32) urows = v;
+        if (v >= 16 && v <= 32 && v % 4 == 0) urows = v;
     }
     int warps = std::min(cap, warps_for(urows));
     if (warps_override > 0) warps = std::min(warps, warps_override);

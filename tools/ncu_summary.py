@@ -84,7 +84,14 @@ def main():
         if a.traffic_json:
             t_i = h.index("gpu__time_duration.sum")
             with open(a.traffic_json, "w") as f:
+                def pct(k):
+                    return float(row[h.index(k)].replace(",", "")) if k in h and row[h.index(k)] else None
+
                 json.dump({"kernel": row[name_i][:100], "dram_bytes_per_launch": rd + wr, "dram_read": rd,
+                           "lts_throughput_pct": pct("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+                           "l1tex_throughput_pct": pct("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                           "issue_active_pct": pct("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                           "l2_hit_rate_pct": pct("lts__t_sector_hit_rate.pct"),
                            "dram_write": wr, "l2_bytes_per_launch": l2, "report": a.rep,
                            "ncu_kernel_time": f"{row[t_i]} {units[t_i]}",
                            # the K1 sources this capture was taken of (bench.py flags stale captures)

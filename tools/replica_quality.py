@@ -30,11 +30,12 @@ def main():
     p.add_argument("--sync", type=int, nargs="+", default=[100_000])
     p.add_argument("--pairs", type=int, default=1 << 20)
     p.add_argument("--kernel", type=int, default=0)
+    p.add_argument("--tokens", type=int, default=0, help="train on this prefix of the corpus (0 = all of it)")
     p.add_argument("--out", default="")
     a = p.parse_args()
     c = CONFIGS[a.config]
-    _, vocab, ids = bench.workload(a.config, 0, 1)
-    ids = bench.host_ids(ids)
+    _, vocab, ids = bench.workload(a.config, 0, 1, device=a.config in ("c4", "c5"))
+    ids = bench.host_ids(ids, a.tokens or None)
     tree = api.build_huffman_tree(vocab)
     sel = api.select_cached_nodes(tree, 31)
     cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=1, sample=c.sample, iterations=c.iterations,
