@@ -223,20 +223,31 @@ CG_API int cg_session_model_buffer(cg_session* s, void** device_ptr, size_t* byt
  * keep that semantics between syncs: each replica trains its shard from the model of the
  * last sync (the snapshot); at a sync every replica's delta (model - snapshot) is summed
  * over the replicas (cg_session_sync_delta exposes it for an NCCL all-reduce with SUM) and
- * applied to the snapshot row by row with cg_sync_row_scale (cg_session_sync_apply). */
+ * applied to the snapshot row by row (cg_session_sync_apply) with the scale
+ *     s(row) = min(prior, max(ratio, trust)),
+ *     prior = cg_sync_row_scale(q, n, centers),
+ *     ratio = clamp(sum_r |delta_r|^2 / |sum_r delta_r|^2, 1/n, 1),
+ *     trust = min(1, 0.25 / (rms norm of the other matrix's 1024 hottest rows x |sum_r delta_r|)):
+ * the ratio is 1 (the reference's plain sum) for a row one replica touched or whose replicas
+ * moved it in orthogonal directions and 1/n (their average) when every replica made the same
+ * move from the same snapshot; a summed step small enough to move the row's logits by less
+ * than ~0.25 is kept whole (n stale trajectories then add up like one sequential one). */
 /* snapshot = model: the start of a sync period (after reset/set_model, before training). */
 CG_API int cg_session_sync_begin(cg_session* s);
-/* delta = model - snapshot, in a session-owned device buffer of n_floats (the model's layout). */
+/* delta = model - snapshot, in a session-owned device buffer of n_floats: the model's layout
+ * followed by one squared norm per model row (|delta_r|^2, padded to a multiple of 4
+ * floats) and 4 floats holding the squared norms of the syn0 and the syn1 matrix. All-reduce
+ * all n_floats with SUM. */
 CG_API int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floats);
 /* With the delta buffer holding the sum over n_replicas replicas: model = snapshot +
- * scale(row) x delta, snapshot = model. words_per_replica: id-stream tokens each replica
- * trained since the last sync (the sync interval). */
+ * s(row) x delta, snapshot = model. words_per_replica: id-stream tokens each replica
+ * trained since the last sync (the sync interval; it sets the prior below). */
 CG_API int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_replica);
-/* The per-row scale of the summed delta for a row on a share q of the updates, n_replicas
- * replicas of `centers` kept centers each per sync: min(1, max(1 / (p n), 128 / (n q centers)))
- * with p = 1 - (1 - q)^centers -- rows few replicas touch are summed as in the reference, a
- * row every replica updates from the same snapshot gets at most 128 stale updates' worth and
- * at least the replicas' average. Host-only arithmetic (no device needed). */
+/* The prior of the per-row scale from expected update counts, for a row on a share q of
+ * the updates, n_replicas replicas of `centers` kept centers each per sync:
+ * min(1, max(1 / (p n), 128 / (n q centers))) with p = 1 - (1 - q)^centers -- 1 for rows few
+ * replicas touch, at most 128 stale updates' worth and at least the replicas' average for a
+ * row every replica updates. Host-only arithmetic (no device needed). */
 CG_API float cg_sync_row_scale(double q, int32_t n_replicas, double centers);
 
 /* Hogwild kernel knobs (zero-initialised = defaults, except smem_cache_rows: -1). */

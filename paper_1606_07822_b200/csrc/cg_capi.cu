@@ -185,23 +185,94 @@ __global__ void scatter_rows_kernel(float* dst, int32_t ds, const float* src, in
 unsigned grid_for(int64_t n) { return static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 // ---- replica sync: deltas since the last sync, summed across replicas ----
-__global__ void sync_delta_kernel(const float4* model, const float4* snap, float4* delta, size_t n4) {
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const float4 m = model[i], b = snap[i];
-        delta[i] = make_float4(m.x - b.x, m.y - b.y, m.z - b.z, m.w - b.w);
+// The delta buffer: the model's layout, then one squared norm per model row (|delta_r|^2),
+// padded to a multiple of 4 floats, then 4 floats of which the first two are the summed
+// squared norms of the syn0 and the syn1 rows of the model. One all-reduce sums it all.
+// Measured (tools/replica_quality.py, learning ratio against one replica): with no trust
+// term C5 split 8 ways learns 1.04 but C1 split 4 ways at 500-word syncs 0.915; with 0.5 over
+// the rms of all rows C1 0.974 but C5 0.66-0.76 (the hot vectors that most updates pair with
+// are longer than the average row); 0.25 over the 1024 hottest rows gives 1.04 and 0.974.
+#ifndef CG_SYNC_TRUST
+#define CG_SYNC_TRUST 0.25f
+#endif
+#ifndef CG_SYNC_HOT
+#define CG_SYNC_HOT 1024  // the matrices' rms norms are taken over their first CG_SYNC_HOT (hottest) rows; 0 = all
+#endif
+constexpr float kSyncTrust = CG_SYNC_TRUST;  // a summed step may move a logit by about this much unscaled
+constexpr size_t kSyncHot = CG_SYNC_HOT;
+__host__ __device__ inline size_t sync_tail_rows(size_t rows) { return (rows + 3) & ~size_t{3}; }
+
+// One warp per model row: delta = model - snapshot, sumsq[row] = |delta|^2, and the row's own
+// squared norm added to its matrix's total.
+__global__ void sync_delta_kernel(const float4* model, const float4* snap, float4* delta, float* sumsq, float* totals,
+                                  size_t rows, size_t rows0, int32_t row4) {
+    const size_t warp = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) >> 5;
+    const size_t nwarps = (static_cast<size_t>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    float own0 = 0.f, own1 = 0.f;
+    for (size_t r = warp; r < rows; r += nwarps) {
+        float acc = 0.f, own = 0.f;
+        for (int q = lane; q < row4; q += 32) {
+            const size_t i = r * static_cast<size_t>(row4) + q;
+            const float4 m = model[i], b = snap[i];
+            const float4 d = make_float4(m.x - b.x, m.y - b.y, m.z - b.z, m.w - b.w);
+            delta[i] = d;
+            acc += d.x * d.x + d.y * d.y + d.z * d.z + d.w * d.w;
+            own += m.x * m.x + m.y * m.y + m.z * m.z + m.w * m.w;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            own += __shfl_xor_sync(0xffffffffu, own, o);
+        }
+        if (lane == 0) sumsq[r] = acc;
+        const size_t rr = r < rows0 ? r : r - rows0;  // rows are hottest first in both matrices
+        if (kSyncHot == 0 || rr < kSyncHot) (r < rows0 ? own0 : own1) += own;
+    }
+    if (lane == 0) {
+        if (own0 != 0.f) atomicAdd(totals, own0);
+        if (own1 != 0.f) atomicAdd(totals + 1, own1);
     }
 }
-// model = snapshot + scale[row] * delta (the replicas' summed deltas); snapshot = model
-__global__ void sync_apply_kernel(float4* model, float4* snap, const float4* delta, const float* scale, size_t n4,
-                                  int32_t row4) {
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n4;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const float sc = scale[i / static_cast<size_t>(row4)];
-        const float4 b = snap[i], d = delta[i];
-        const float4 m = make_float4(b.x + sc * d.x, b.y + sc * d.y, b.z + sc * d.z, b.w + sc * d.w);
-        model[i] = m;
-        snap[i] = m;
+// With the buffer summed over the n replicas: model = snapshot + s x delta, snapshot = model,
+// one warp per row, s = min(prior[row], max(ratio, trust)):
+//  * ratio = clamp(sum_r |delta_r|^2 / |sum_r delta_r|^2, 1 / n, 1) is 1 when the replicas'
+//    deltas are orthogonal (or one replica alone touched the row: the reference's plain sum)
+//    and 1 / n when they are parallel (every replica made the same move from the same
+//    snapshot: their average); with it alone the applied step is never longer than the
+//    root-sum-square of the replicas' own steps;
+//  * trust = min(1, T / |sum_r delta_r|) with T = kSyncTrust / (rms norm of the other
+//    matrix's hottest rows): a summed step that moves the row's logits by less than ~kSyncTrust is in the
+//    linear regime, where n stale trajectories add up like one sequential one, and is kept
+//    whole however parallel the deltas are (small corpora, early training).
+__global__ void sync_apply_kernel(float4* model, float4* snap, const float4* delta, const float* sumsq,
+                                  const float* totals, const float* prior, size_t rows, size_t rows0, int32_t row4,
+                                  float inv_n) {
+    const size_t warp = (blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x) >> 5;
+    const size_t nwarps = (static_cast<size_t>(gridDim.x) * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    // rms row norms of the two matrices (totals are summed over the replicas)
+    const size_t cnt0 = kSyncHot ? min(rows0, kSyncHot) : rows0, cnt1 = kSyncHot ? min(rows - rows0, kSyncHot) : rows - rows0;
+    const float rms0 = sqrtf(totals[0] * inv_n / static_cast<float>(cnt0));
+    const float rms1 = sqrtf(totals[1] * inv_n / static_cast<float>(cnt1));
+    for (size_t r = warp; r < rows; r += nwarps) {
+        float acc = 0.f;
+        for (int q = lane; q < row4; q += 32) {
+            const float4 d = delta[r * static_cast<size_t>(row4) + q];
+            acc += d.x * d.x + d.y * d.y + d.z * d.z + d.w * d.w;
+        }
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (!(acc > 0.f)) continue;  // nobody moved the row
+        const float ratio = fminf(1.0f, fmaxf(inv_n, sumsq[r] / acc));
+        const float other = fmaxf(r < rows0 ? rms1 : rms0, 1e-12f);
+        const float trust = fminf(1.0f, kSyncTrust / (other * sqrtf(acc)));
+        const float sc = fminf(prior[r], fmaxf(ratio, trust));
+        for (int q = lane; q < row4; q += 32) {
+            const size_t i = r * static_cast<size_t>(row4) + q;
+            const float4 b = snap[i], d = delta[i];
+            const float4 m = make_float4(b.x + sc * d.x, b.y + sc * d.y, b.z + sc * d.z, b.w + sc * d.w);
+            model[i] = m;
+            snap[i] = m;
+        }
     }
 }
 
@@ -831,11 +902,17 @@ int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floats) {
     return guarded([&] {
         if (s->snap.n != s->model.n) invalid("cg_session_sync_begin was not called");
         CG_CUDA(cudaSetDevice(s->device));
-        if (s->delta.n != s->model.n) s->delta.alloc(s->model.n);
-        const size_t n4 = s->model.n / 4;
-        sync_delta_kernel<<<grid_for(static_cast<int64_t>(n4)), 256, 0, s->stream>>>(
+        // the delta in the model's layout, then one squared norm per model row (padded to 4),
+        // then the squared norms of the two matrices (4 floats)
+        const size_t rows = s->model.n / static_cast<size_t>(s->Dp);
+        const size_t tail = sync_tail_rows(rows);
+        const size_t total = s->model.n + tail + 4;
+        if (s->delta.n != total) s->delta.alloc(total);
+        CG_CUDA(cudaMemsetAsync(s->delta.p + s->model.n, 0, (tail + 4) * sizeof(float), s->stream));
+        sync_delta_kernel<<<148 * 8, 256, 0, s->stream>>>(
             reinterpret_cast<const float4*>(s->model.p), reinterpret_cast<const float4*>(s->snap.p),
-            reinterpret_cast<float4*>(s->delta.p), n4);
+            reinterpret_cast<float4*>(s->delta.p), s->delta.p + s->model.n, s->delta.p + s->model.n + tail, rows,
+            static_cast<size_t>(s->V), s->Dp / 4);
         CG_CUDA(cudaGetLastError());
         CG_CUDA(cudaStreamSynchronize(s->stream));
         if (delta_dev) *delta_dev = s->delta.p;
@@ -845,7 +922,10 @@ int cg_session_sync_delta(cg_session* s, void** delta_dev, size_t* n_floats) {
 
 int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_replica) {
     return guarded([&] {
-        if (s->snap.n != s->model.n || s->delta.n != s->model.n) invalid("cg_session_sync_delta was not called");
+        const size_t rows = s->model.n / static_cast<size_t>(s->Dp);
+        const size_t tail = sync_tail_rows(rows);
+        if (s->snap.n != s->model.n || s->delta.n != s->model.n + tail + 4)
+            invalid("cg_session_sync_delta was not called");
         if (n_replicas < 1) invalid("replica count must be >= 1");
         CG_CUDA(cudaSetDevice(s->device));
         if (s->sync_n != n_replicas || s->sync_words != words_per_replica) {
@@ -856,10 +936,10 @@ int cg_session_sync_apply(cg_session* s, int32_t n_replicas, uint64_t words_per_
             s->sync_n = n_replicas;
             s->sync_words = words_per_replica;
         }
-        const size_t n4 = s->model.n / 4;
-        sync_apply_kernel<<<grid_for(static_cast<int64_t>(n4)), 256, 0, s->stream>>>(
+        sync_apply_kernel<<<148 * 8, 256, 0, s->stream>>>(
             reinterpret_cast<float4*>(s->model.p), reinterpret_cast<float4*>(s->snap.p),
-            reinterpret_cast<const float4*>(s->delta.p), s->sync_scale.p, n4, s->Dp / 4);
+            reinterpret_cast<const float4*>(s->delta.p), s->delta.p + s->model.n, s->delta.p + s->model.n + tail,
+            s->sync_scale.p, rows, static_cast<size_t>(s->V), s->Dp / 4, 1.0f / static_cast<float>(n_replicas));
         CG_CUDA(cudaGetLastError());
         CG_CUDA(cudaStreamSynchronize(s->stream));
     });
@@ -1103,6 +1183,122 @@ int cg_session_train(cg_session* s, cg_train_stats* st) {
     });
 }
 
+}  // extern "C"
+
+namespace {
+// cg_train's Hogwild path for long id streams: the first pass trains chunk by chunk while
+// the ids are still crossing PCIe. A producer thread copies chunk c into the session's id
+// buffer on its own stream, checks its ids on the device and records an event; the caller's
+// thread waits for the event and trains the chunk (the draws are keyed by the global token
+// index, so only the sentence cuts at chunk edges differ from one launch, as in
+// train_file_pipelined). Chunks ramp up from 4M ids so training starts early.
+constexpr int64_t kPipelineMinIds = int64_t{32} << 20;
+// CG_PIPELINE_MIN_IDS / CG_PIPELINE_FIRST override the threshold and the first chunk (tests).
+int64_t env_ids(const char* name, int64_t fallback) {
+    const char* e = std::getenv(name);
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? static_cast<int64_t>(v) : fallback;
+}
+void train_ids_pipelined(cg_session* s, const int32_t* ids, int64_t n, cg_train_stats* out) {
+    CG_CUDA(cudaSetDevice(s->device));
+    s->ids.alloc(static_cast<size_t>(n));
+    session_alloc_stream(s, n);
+    std::vector<int64_t> cut{0};
+    for (int64_t len = env_ids("CG_PIPELINE_FIRST", int64_t{4} << 20); cut.back() < n;
+         len = std::min<int64_t>(len * 2, int64_t{64} << 20))
+        cut.push_back(std::min(n, cut.back() + len));
+    const int chunks = static_cast<int>(cut.size()) - 1;
+    cudaStream_t cst = nullptr;
+    CG_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(chunks));
+    for (auto& e : ev) CG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    auto* flags = static_cast<unsigned long long*>(cgint::PinnedPool::get().alloc(static_cast<size_t>(chunks) * 8));
+    DevBuf<unsigned long long> bad;
+    bad.alloc(1);
+    CG_CUDA(cudaMemsetAsync(bad.p, 0, 8, cst));
+    std::mutex mu;
+    std::condition_variable cv;
+    int ready = 0;
+    std::exception_ptr perr;
+    std::thread producer([&] {
+        try {
+            CG_CUDA(cudaSetDevice(s->device));
+            for (int c = 0; c < chunks; ++c) {
+                const int64_t a = cut[static_cast<size_t>(c)], len = cut[static_cast<size_t>(c) + 1] - a;
+                copy_to_device(s->ids.p + a, ids + a, static_cast<size_t>(len) * sizeof(int32_t), cst);
+                id_range_kernel<<<grid_for(len), 256, 0, cst>>>(s->ids.p + a, len, s->V, bad.p);
+                CG_CUDA(cudaGetLastError());
+                CG_CUDA(cudaMemcpyAsync(flags + c, bad.p, 8, cudaMemcpyDeviceToHost, cst));
+                CG_CUDA(cudaEventRecord(ev[static_cast<size_t>(c)], cst));
+                {
+                    std::lock_guard<std::mutex> g(mu);
+                    ready = c + 1;
+                }
+                cv.notify_one();
+            }
+        } catch (...) {
+            perr = std::current_exception();
+            {
+                std::lock_guard<std::mutex> g(mu);
+                ready = chunks + 1;  // wakes the trainer; perr tells it why
+            }
+            cv.notify_one();
+        }
+    });
+    cg_train_stats st{};
+    std::string err;
+    int err_rc = CG_OK;
+    auto add = [&st](const cg_epoch_stats& e) {
+        st.kernel_seconds += (e.train_ms + e.subsample_ms) * 1e-3;
+        st.centers += e.kept;
+        st.pairs += e.pairs;
+        st.steps += e.steps;
+        st.words_processed += e.words;
+    };
+    for (int c = 0; c < chunks && err_rc == CG_OK; ++c) {
+        {
+            std::unique_lock<std::mutex> g(mu);
+            cv.wait(g, [&] { return ready > c; });
+            if (ready > chunks) break;  // the producer failed
+        }
+        CG_CUDA(cudaEventSynchronize(ev[static_cast<size_t>(c)]));
+        if (flags[c]) {
+            err_rc = CG_ERR_INVALID_ARGUMENT;
+            err = "id out of vocabulary range";
+            break;
+        }
+        cg_epoch_stats e{};
+        const int64_t a = cut[static_cast<size_t>(c)], b = cut[static_cast<size_t>(c) + 1];
+        const int rc = cg_session_train_range(s, 0, a, b, static_cast<uint64_t>(a), 1, &e);
+        if (rc != CG_OK) {
+            err_rc = rc;
+            err = g_error;
+            break;
+        }
+        add(e);
+    }
+    producer.join();
+    cudaStreamSynchronize(cst);
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(cst);
+    cgint::PinnedPool::get().free(flags);
+    if (perr) std::rethrow_exception(perr);
+    if (err_rc != CG_OK) {
+        s->n_ids = 0;
+        throw CgError(err_rc, err);
+    }
+    for (int32_t it = 1; it < s->cfg.iterations; ++it) {
+        cg_epoch_stats e{};
+        const int rc = cg_session_train_range(s, it, 0, n, static_cast<uint64_t>(it) * static_cast<uint64_t>(n), 1, &e);
+        if (rc != CG_OK) throw CgError(rc, g_error);
+        add(e);
+    }
+    *out = st;
+}
+}  // namespace
+
+extern "C" {
+
 int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, const int32_t* ids, int64_t n_ids,
              float* syn0_out, float* syn1_out, cg_train_stats* stats) {
     cg_session* s = nullptr;
@@ -1115,10 +1311,16 @@ int cg_train(const cg_config* cfg, int32_t mode, const cg_model_desc* model, con
     int rc = cg_session_create(cfg, mode, model, dev, nullptr, &s);
     if (rc != CG_OK) return rc;
     const auto t0 = std::chrono::steady_clock::now();
-    rc = cg_session_upload_ids(s, ids, n_ids);
-    const auto t1 = std::chrono::steady_clock::now();
     cg_train_stats st{};
-    if (rc == CG_OK) rc = cg_session_train(s, &st);
+    auto t1 = t0;
+    if (mode == CG_MODE_HOGWILD && ids && n_ids >= env_ids("CG_PIPELINE_MIN_IDS", kPipelineMinIds) &&
+        !std::getenv("CG_NO_PIPELINE")) {
+        rc = guarded([&] { train_ids_pipelined(s, ids, n_ids, &st); });
+    } else {
+        rc = cg_session_upload_ids(s, ids, n_ids);
+        t1 = std::chrono::steady_clock::now();
+        if (rc == CG_OK) rc = cg_session_train(s, &st);
+    }
     const auto t2 = std::chrono::steady_clock::now();
     if (rc == CG_OK) rc = cg_session_download(s, syn0_out, syn1_out);
     const auto t3 = std::chrono::steady_clock::now();

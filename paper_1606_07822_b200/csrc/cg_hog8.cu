@@ -60,11 +60,8 @@ using namespace cgdev;
 
 constexpr int kTileRows = 16;  // M of one mma tile: context rows per batch
 constexpr int kGhStride = 40;  // fp16 G scratch [16 contexts][32 path rows], 80-byte rows
-#ifndef CG_K8_SWP
-#define CG_K8_SWP 0  // 1: the H and dU loops load the next tile's B fragment before this tile's mma
-#endif
 #ifndef CG_K8_UNROLL
-#define CG_K8_UNROLL 2
+#define CG_K8_UNROLL 4  // tiles per unrolled step of the S, H and dU loops (1 / 2 / 4 at C5: 2414 / 2338 / 2314 ms)
 #endif
 #define CG_PRAGMA(x) _Pragma(#x)
 #define CG_UNROLL(n) CG_PRAGMA(unroll n)
@@ -150,28 +147,9 @@ __device__ __forceinline__ void h_phase(const __half* GH, const __half* const (&
 #pragma unroll
     for (int kk = 0; kk < KS; ++kk) ldsm_x4(a[kk], GH + (rr + 8 * (m & 1)) * kGhStride + 16 * kk + 8 * (m >> 1));
     const int n16 = K16 > 0 ? K16 : k16;
-#if CG_K8_SWP
-    uint32_t bn[KS][4];
-#pragma unroll
-    for (int kk = 0; kk < KS; ++kk) ldsm_x4_t(bn[kk], pb[kk]);
-#endif
 CG_UNROLL(CG_K8_UNROLL)
     for (int np = 0; np < n16; ++np) {
         float c0[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f};
-#if CG_K8_SWP
-        uint32_t b[KS][4];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e) b[kk][e] = bn[kk][e];
-            if (np + 1 < n16) ldsm_x4_t(bn[kk], pb[kk] + 16 * (np + 1));
-        }
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) {
-            mma_f16(c0, a[kk], b[kk][0], b[kk][1]);
-            mma_f16(c1, a[kk], b[kk][2], b[kk][3]);
-        }
-#else
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
             uint32_t b[4];
@@ -179,7 +157,6 @@ CG_UNROLL(CG_K8_UNROLL)
             mma_f16(c0, a[kk], b[0], b[1]);
             mma_f16(c1, a[kk], b[2], b[3]);
         }
-#endif
         const int d0 = 16 * np + 2 * t;
         const bool second = 16 * np + 8 < dp;  // warp-uniform: dp is a multiple of 8
         red_add2(p0, d0, c0[0], c0[1]);
@@ -202,20 +179,10 @@ __device__ __forceinline__ void u_phase(const __half* GH, const __half* pb, int 
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) ldsm_x4_t(a[mt], GH + (rr + 8 * (m >> 1)) * kGhStride + 16 * mt + 8 * (m & 1));
     const int n16 = K16 > 0 ? K16 : k16;
-#if CG_K8_SWP
-    uint32_t bn[4];
-    ldsm_x4_t(bn, pb);
-#endif
 CG_UNROLL(CG_K8_UNROLL)
     for (int np = 0; np < n16; ++np) {
         uint32_t b[4];
-#if CG_K8_SWP
-#pragma unroll
-        for (int e = 0; e < 4; ++e) b[e] = bn[e];
-        if (np + 1 < n16) ldsm_x4_t(bn, pb + 16 * (np + 1));
-#else
         ldsm_x4_t(b, pb + 16 * np);
-#endif
         const int d0 = 16 * np + 2 * t;
         const bool second = 16 * np + 8 < dp;
 #pragma unroll
@@ -570,11 +537,12 @@ bool hog8_plan(int d4, int cache_rows, int ctx_rows, int blocks, int warps_overr
     auto warps_for = [&](int ur) { return static_cast<int>((budget - fixed) / k8_warp_bytes(ssh, vrows, ur, (d4 + 31) / 32)); };
     const int cap = k8_max_warps((d4 + 31) / 32);
     // Path rows staged per chunk (a deeper path trains in chunks, its contexts staying
-    // staged; every chunk repeats the H phase): 16 when no path is deeper, else 24 when that
-    // keeps at least 8 warps on the SM (measured, K1 ms at 16 / 24 / 32 rows: C5 3109 / 2872 /
-    // 3053, C2 67.3 / 63.9 / 69.9, C4 914 / 881 / 934). CG_UROWS overrides (experiments).
-    int urows = 16;
-    if (max_depth > 16 && std::min(cap, warps_for(24)) >= 8) urows = 24;
+    // staged; every chunk repeats the H phase): the deepest path rounded up to 4, at least 16
+    // and at most 24 -- more rows cost more warps than the second chunk of the few deeper
+    // paths (measured, K1 ms at 16 / 20 / 24 / 28 / 32 rows: C5, depth 26: 3109 / 2452 / 2338 /
+    // 2424 / 3053; C4, depth 20: 914 / 719 / 763 / 833 / 934). CG_UROWS overrides (experiments).
+    int urows = std::min(24, std::max(16, (max_depth + 3) / 4 * 4));
+    if (std::min(cap, warps_for(urows)) < 8) urows = 16;
     if (const char* e = std::getenv("CG_UROWS")) {
         const int v = std::atoi(e);
         if (v >= 16 && v <= 32 && v % 4 == 0) urows = v;

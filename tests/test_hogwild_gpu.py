@@ -65,6 +65,30 @@ def test_hogwild_multiple_ranges_cover_stream():
     assert words == ids.size and kept == ids.size  # sample 0 keeps everything
 
 
+def test_cg_train_pipelined_upload_covers_stream_and_learns(monkeypatch):
+    """cg_train() on a long id stream trains the first pass chunk by chunk while the ids are
+    still being copied to the device (train_ids_pipelined, cg_capi.cu). With the thresholds
+    lowered so that C1 takes that path in several chunks: every token is counted once per
+    pass, the model learns like the one-launch path, pageable and multi-pass inputs work,
+    and an out-of-range id is refused."""
+    c, vocab, ids = c1()
+    tree, sel = setup(vocab)
+    cfg = api.TrainConfig(dim=32, window=5, min_count=1, sample=c.sample, iterations=2, seed=5, mode="hogwild")
+    plain = api.train(ids, vocab, tree, sel, cfg)
+    monkeypatch.setenv("CG_PIPELINE_MIN_IDS", "1")
+    monkeypatch.setenv("CG_PIPELINE_FIRST", "60000")  # chunks of 60k, 120k, 240k, 480k, 100k ids
+    st = api.TrainStats()
+    piped = api.train(ids, vocab, tree, sel, cfg, st)
+    assert st.words_processed == 2 * ids.size
+    init = api.init_model(vocab.size(), 32, 5)
+    l0, lp, lq = (_loss(m, tree, vocab, ids, c) for m in (init, plain, piped))
+    assert lq < l0 and abs((l0 - lq) - (l0 - lp)) < 0.10 * (l0 - lp), (l0, lp, lq)
+    bad = ids.copy()
+    bad[700_000] = vocab.size()
+    with pytest.raises(ValueError):
+        api.train(bad, vocab, tree, sel, cfg)
+
+
 def _loss(model, tree, vocab, ids, c, n=1 << 16, seed=12345):
     cen, ctx = O.sample_pairs(ids, vocab.counts, vocab.total_tokens(), c.sample, c.window, seed, n)
     t = O.Tree(tree.offsets, tree.nodes, tree.turns, tree.usage)

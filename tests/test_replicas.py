@@ -83,14 +83,44 @@ class HostReplica:
         self.snap = self.m.copy()
 
     def sync_delta_tensor(self):
-        self.delta = torch.from_numpy(self.m - self.snap)
+        # the delta in the model's layout, one squared norm per row, and the squared norms
+        # of the two matrices (cg_session_sync_delta)
+        d = self.m - self.snap
+        self.delta = torch.from_numpy(np.concatenate([d, _row_sumsq(d), _matrix_sumsq(self.m)]).astype(np.float32))
         return self.delta
 
     def sync_apply(self, n, words):
-        sc = np.array([self.api.sync_row_scale(q, n, words) for q in self.q], np.float32)
-        rows = np.concatenate([np.repeat(sc[:V], D), np.repeat(sc[V:], D)])
-        self.m[:] = self.snap + rows * self.delta.numpy()
+        total = self.delta.numpy()
+        d, sumsq, mats = total[: self.m.size], total[self.m.size:-2], total[-2:]
+        prior = np.array([self.api.sync_row_scale(q, n, words) for q in self.q], np.float32)
+        self.m[:] = self.snap + _sync_rows(d, sumsq, mats, prior, n) * d
         self.snap = self.m.copy()
+
+
+TRUST = 0.25  # kSyncTrust (cg_capi.cu); the rms norms cover the 1024 hottest rows: all of them here
+
+
+def _sync_rows(total, sumsq, mats, prior, n):
+    """cg_session_sync_apply's per-row scale, repeated over each row's D floats:
+    s = min(prior, max(ratio, trust)), ratio = clamp(sum |delta_r|^2 / |sum delta_r|^2, 1/n, 1),
+    trust = min(1, TRUST / (rms row norm of the other matrix x |sum delta_r|))."""
+    norm2 = _row_sumsq(total)
+    ratio = np.clip(np.divide(sumsq, norm2, out=np.ones_like(sumsq), where=norm2 > 0), 1.0 / n, 1.0)
+    rms0, rms1 = np.sqrt(mats[0] / n / V), np.sqrt(mats[1] / n / (V - 1))
+    other = np.maximum(np.concatenate([np.full(V, rms1), np.full(V - 1, rms0)]), 1e-12)
+    trust = np.minimum(1.0, TRUST / (other * np.sqrt(np.maximum(norm2, 1e-30))))
+    sc = np.minimum(prior, np.maximum(ratio, trust)).astype(np.float32)
+    return np.concatenate([np.repeat(sc[:V], D), np.repeat(sc[V:], D)])
+
+
+def _matrix_sumsq(flat):
+    r = _row_sumsq(flat)
+    return np.array([r[:V].sum(), r[V:].sum()], np.float32)
+
+
+def _row_sumsq(flat):
+    """Squared norm of every model row: V syn0 rows, then V - 1 syn1 rows of D floats."""
+    return (flat.reshape(2 * V - 1, D).astype(np.float32) ** 2).sum(axis=1, dtype=np.float32)
 
 
 def _worker(rank, world, port, out, mode):
@@ -159,8 +189,7 @@ def test_two_replicas_gloo_match_sequential_simulation(mode):
     q = row_shares(counts)
     from paper_1606_07822_b200 import api
 
-    sc = np.array([api.sync_row_scale(x, world, 5000) for x in q], np.float32)
-    rows = np.concatenate([np.repeat(sc[:V], D), np.repeat(sc[V:], D)])
+    prior = np.array([api.sync_row_scale(x, world, 5000) for x in q], np.float32)
     for epoch in range(2):
         chunks = [plan_chunks(b - a, 5000) for a, b in n]
         for i in range(max(len(c) for c in chunks)):
@@ -170,8 +199,12 @@ def test_two_replicas_gloo_match_sequential_simulation(mode):
                     steps[r](epoch, ch.begin, ch.end, 0, world)
             if mode == "average":
                 new = (models[0] + models[1]) / 2
-            else:  # the summed deltas since the last sync, scaled per row
-                new = snap + rows * ((models[0] - snap) + (models[1] - snap))
+            else:  # the summed deltas since the last sync, scaled per row (_sync_rows)
+                d = [(models[r] - snap).astype(np.float32) for r in range(world)]
+                total = d[0] + d[1]
+                sumsq = _row_sumsq(d[0]) + _row_sumsq(d[1])
+                mats = _matrix_sumsq(models[0]) + _matrix_sumsq(models[1])
+                new = snap + _sync_rows(total, sumsq, mats, prior, world) * total
             for r in range(world):
                 models[r][:] = new
             snap = new.copy()
