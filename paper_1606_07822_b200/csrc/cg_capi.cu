@@ -289,6 +289,7 @@ struct cg_session {
     int32_t V = 0, D = 0, Dp = 0, K = 0;
     int64_t total_tokens = 0;
     int32_t max_depth = 0;
+    int32_t cover_depth = 0;  // path length that covers 90% of the kept centers (v8 stages this many path rows)
 
     // host layout maps (hogwild): node id -> device row and back
     std::vector<int32_t> row_of_node, node_of_row;
@@ -658,6 +659,26 @@ int cg_session_create(const cg_config* cfg, int32_t mode, const cg_model_desc* m
                 if (w < static_cast<int32_t>(kept.size())) kept[static_cast<size_t>(w)] = k;
             }
             for (double k : kept) s->ctx_share.push_back(std::min(1.0, (cfg->window + 1) * k / std::max(kept_total, 1.0)));
+            {  // the path length that 90% of the kept centers stay within: v8 stages that many
+               // path rows per warp and trains the few deeper paths in a second chunk (measured:
+               // C4, deepest path 22, 719 ms with 20 staged rows and 9 warps per SM against 753
+               // with 24 and 8; C5, deepest 26, 90% within 24: 2338 ms with 24, 2452 with 20)
+                std::vector<double> by_len(static_cast<size_t>(s->max_depth) + 1, 0.0);
+                for (int32_t w = 0; w < V; ++w) {
+                    const double kpw = kp.empty() ? 1.0 : std::min(1.0, static_cast<double>(kp[static_cast<size_t>(w)]));
+                    by_len[static_cast<size_t>(md->path_offsets[w + 1] - md->path_offsets[w])] +=
+                        static_cast<double>(md->counts[w]) * kpw;
+                }
+                double run = 0.0;
+                s->cover_depth = s->max_depth;
+                for (int32_t len = 0; len <= s->max_depth; ++len) {
+                    run += by_len[static_cast<size_t>(len)];
+                    if (run >= 0.9 * kept_total) {
+                        s->cover_depth = len;
+                        break;
+                    }
+                }
+            }
             if (mode == CG_MODE_HOGWILD) {
                 s->row_q.assign(2 * static_cast<size_t>(V), 0.0f);
                 for (int32_t w = 0; w < V; ++w) {
@@ -1041,7 +1062,7 @@ int cg_session_train_range(cg_session* s, int32_t epoch, int64_t tok_begin, int6
             // v8 (tensor cores) unless the caller asked for v5 (FP32 FMA) or the rows are too wide
             auto plan_tc = [&](int32_t rows, int32_t ctx) {
                 return s->tune.kernel != 5 && cgk::hog8_plan(s->Dp / 4, rows, ctx, blocks, s->tune.warps_per_block,
-                                                             s->tune.centers_per_warp, n, s->max_depth, s->cfg.window, &g);
+                                                             s->tune.centers_per_warp, n, s->cover_depth, s->cfg.window, &g);
             };
             bool v8 = plan_tc(std::min<int32_t>(s->K, cgk::kMaxCacheRows), 0);
             const double inflight =
