@@ -44,6 +44,8 @@ def main():
     p.add_argument("--ref-tokens", type=int, default=20_000_000, help="reference sample per K (0 = skip)")
     p.add_argument("--out", default="")
     p.add_argument("--kernel", type=int, default=0, help="K1 version (cg_tuning.kernel; 0 = default)")
+    p.add_argument("--min-cache-rows", type=int, default=0,
+                   help="cg_tuning.min_cache_rows: 0 = the stability floor, < 0 = none (K honoured literally)")
     a = p.parse_args()
 
     import torch
@@ -65,8 +67,8 @@ def main():
         cfg = api.TrainConfig(dim=c.dim, window=c.window, min_count=c.min_count, sample=c.sample, iterations=1,
                               cache_nodes=k, seed=c.seed, mode="hogwild")
         sess = api.Session(vocab, tree, sel, cfg)
-        if a.kernel:
-            sess.tune(kernel=a.kernel)
+        if a.kernel or a.min_cache_rows:
+            sess.tune(kernel=a.kernel, min_cache_rows=a.min_cache_rows)
         if isinstance(ids, np.ndarray):
             sess.upload_ids(ids)
         else:
