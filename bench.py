@@ -6,7 +6,10 @@ corpus. Default: BASELINE config 5 (the largest single-GPU configuration: 1B tok
 Zipf(1.2) over a 1M vocabulary, D 300, W 5, sample 1e-5, K 31 -- the reference default,
 BASELINE.json leaves it to the K sweep). Inputs (id stream, tree, model) are resident in
 HBM before the timed region. Each timed step = K3 subsampling/pair generation + K1
-Hogwild training (+ the replicas' delta sync at N > 1).
+Hogwild training (+ the replicas' delta sync at N > 1). K1 is the library's default
+kernel (v8: each center's products on the tensor cores, fp16-rounded operands, fp32 sums,
+fp32 model and updates; `dtype` says so); the same step on the all-FP32 kernel (v5) is
+timed in the same run and reported as `fp32_kernel`.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
