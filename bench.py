@@ -547,7 +547,11 @@ def main():
             threads = cpu_threads()
             sample = args.cpu_sample_tokens or auto_sample(c)
             rates, walls, n = run_reference(c, vocab, ids, threads, sample, 1, args.cache_nodes)
-            cpu = {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference",
+            extra = {}
+            if args.config == "c1" and threads != 4:  # BASELINE config 1 states 4 CPU threads in the reference
+                r4, _, _ = run_reference(c, vocab, ids, 4, sample, 1, args.cache_nodes)
+                extra = {"value_4_threads": float(np.median(r4))}
+            cpu = {"value": float(np.median(rates)), "unit": UNIT, "cores": threads, "kind": "reference", **extra,
                    "host": cpu_topology(),
                    "sample": f"first {n} tokens of the {args.config} corpus, 1 pass, reference train() "
                              f"(headers compiled unchanged, -O3) with workers={threads}"}
